@@ -1,0 +1,190 @@
+// gb_device.cuh -- device-side constants and arithmetic for the B200
+// Goldbach verifier (sm_100a).  See DESIGN.md for the data layout.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace gbk {
+
+// ---------------------------------------------------------------- geometry
+// A "block" is the unit one CTA sieves and checks: W odd cells (bits) in
+// shared memory.  Cell w of a block covers the odd q = q_w + 2w.  The top
+// JH cells of the window below the first even's q-top form the Phase 1
+// halo: even n checks candidates p = 3 + 2j, j < JH (p <= 8193), against the
+// cell of n - p.  Evens whose minimal p is not found in-tile are handed to
+// the straggler kernel (K4), which continues the same ascending scan.
+constexpr int JH = 4096;                // in-tile Phase 1 candidates j < JH
+constexpr int NWIN = JH / 64;           // 64-candidate windows
+constexpr int W_LOG2 = 19;
+constexpr uint32_t W = 1u << W_LOG2;    // cells per block window
+constexpr uint32_t E = W - JH;          // evens per block
+constexpr int TILE_WORDS = W / 32;      // u32 words of the window
+constexpr int THREADS = 512;            // threads per CTA of the fused kernel
+constexpr int NWARPS = THREADS / 32;
+constexpr uint32_t P_TILE_MAX = 1u << 22; // base primes above: K_large (global strikes)
+constexpr uint32_t P_WARP_MAX = 1024;     // primes below: warp-cooperative strikes
+constexpr uint32_t FIRST_STRIKE_P = 53;   // primes below are in the presieve patterns
+constexpr uint32_t MAX_SEG_EVENS = 1u << 31; // device sub-segment limit
+
+// presieve pattern groups (products of small odd primes); pattern bit k is 0
+// iff 2k+1 is divisible by a prime of the group.  Stored with 64 bits of
+// wrap-around so a 32-bit window at any phase is two word loads.
+__host__ __device__ constexpr uint32_t pg_p(int g) {
+    return g == 0 ? 15015u : g == 1 ? 7429u : g == 2 ? 33263u : 82861u; // 3·5·7·11·13, 17·19·23, 29·31·37, 41·43·47
+}
+__host__ __device__ constexpr uint32_t pat_words(uint32_t P) { return (P + 64 + 31) / 32 + 1; }
+__host__ __device__ constexpr uint32_t pg_off(int g) {
+    return (g > 0 ? pat_words(pg_p(0)) : 0u) + (g > 1 ? pat_words(pg_p(1)) : 0u) +
+           (g > 2 ? pat_words(pg_p(2)) : 0u) + (g > 3 ? pat_words(pg_p(3)) : 0u);
+}
+constexpr uint32_t PAT_WORDS = pg_off(4);
+__host__ __device__ constexpr uint32_t pat_prime(int t) {
+    return t == 0 ? 3u : t == 1 ? 5u : t == 2 ? 7u : t == 3 ? 11u : t == 4 ? 13u : t == 5 ? 17u
+         : t == 6 ? 19u : t == 7 ? 23u : t == 8 ? 29u : t == 9 ? 31u : t == 10 ? 37u
+         : t == 11 ? 41u : t == 12 ? 43u : 47u;
+}
+constexpr int N_PAT_PRIMES = 14;
+
+// straggler list entry flags
+constexpr uint32_t F_NEED_P1 = 1u;      // continue Phase 1 from j_next
+constexpr uint32_t F_P1_FAIL = 2u;      // Phase 1 exhausted: unverified
+constexpr uint32_t F_INJECT = 4u;       // n == inject_fail
+constexpr uint32_t F_OBSERVED = 8u;     // Phase 1 p already observed in-tile
+
+struct StragEntry {
+    uint32_t slot;
+    uint32_t i_seg;   // even index within the segment
+    uint32_t j_next;  // next candidate index (p = 3 + 2j)
+    uint32_t flags;
+};
+
+struct StragResult {
+    uint64_t p1;      // Phase 1 minimal p found by K4 (0 = none)
+    uint64_t p2;      // Phase 2 minimal p (0 = none / not run)
+};
+
+// Device-side per-segment job (one per batch slot).
+struct SegJob {
+    uint64_t a, b;          // evens [a, b]
+    uint64_t qbase;         // q of cell 0 of block b1 (see b1)
+    uint32_t evens;         // (b - a)/2 + 1  (<= MAX_SEG_EVENS)
+    uint32_t nblocks;       // ceil(evens / E)
+    uint32_t block_prefix;  // flat index of this slot's first block
+    uint32_t b1;            // 1 if block 0 is the low block (window at q = 1)
+    uint32_t qg_words;      // words of the large-prime bitmask (0 = none)
+    uint32_t pad;
+};
+
+// Per-slot accumulator written by the kernels.
+struct SlotAcc {
+    unsigned long long sum;     // Σ p (tile-certified)
+    unsigned long long hash;    // Σ p·(n>>1)
+    unsigned long long key;     // max (p << 32 | ~i) over tile-certified evens
+    unsigned long long pad;
+};
+
+// ---------------------------------------------------------------- helpers
+__host__ __device__ __forceinline__ uint64_t first_cell_u64(uint64_t q_w, uint64_t p) {
+    // Cell (relative to odd q_w) of the first odd multiple of p that is
+    // >= max(p^2, q_w): first_tile_index semantics (sieve.cpp:72-89) without
+    // ever forming q_w + d, so it cannot wrap near 2^64.
+    uint64_t pp = p * p; // p < 2^32
+    if (pp >= q_w) return (pp - q_w) >> 1;
+    uint64_t r = q_w % p;
+    uint64_t d = r ? p - r : 0;
+    if (d & 1) d += p;
+    return d >> 1;
+}
+
+// x mod p for p >= 1024, x < 2^32, via an fp32 reciprocal estimate; the
+// estimate is off by at most 2, fixed by the correction loops.
+__device__ __forceinline__ uint32_t mod_fp(uint32_t x, uint32_t p, float rp) {
+    uint32_t q = __float2uint_rz(__uint2float_rz(x) * rp);
+    int32_t r = (int32_t)(x - q * p);
+    while (r < 0) r += (int32_t)p;
+    while (r >= (int32_t)p) r -= (int32_t)p;
+    return (uint32_t)r;
+}
+
+// ------------------------------------------------ Miller-Rabin (K4)
+// Deterministic for n < 2^64 with witnesses {2..37}: the same decision
+// procedure as is_prime_u64 (primality.cpp:32-52), with Montgomery
+// multiplication in place of the 128-bit '%'.
+struct Mont {
+    uint64_t n, ninv, r1; // r1 = 2^64 mod n (Montgomery 1)
+};
+
+__device__ __forceinline__ uint64_t mont_mul(uint64_t a, uint64_t b, const Mont& m) {
+    uint64_t lo = a * b, hi = __umul64hi(a, b);
+    uint64_t q = lo * m.ninv;
+    uint64_t mhi = __umul64hi(q, m.n);
+    // lo + q*n == 0 mod 2^64; carry out of the low half is (lo != 0)
+    uint64_t c = lo != 0;
+    uint64_t r = hi + mhi;
+    bool ov = r < hi;
+    uint64_t r2 = r + c;
+    ov |= r2 < r;
+    if (ov || r2 >= m.n) r2 -= m.n;
+    return r2;
+}
+
+__device__ __forceinline__ Mont mont_init(uint64_t n) {
+    Mont m;
+    m.n = n;
+    uint64_t x = n; // n*x == 1 mod 2^3 for odd n
+    for (int i = 0; i < 5; ++i) x *= 2 - n * x;
+    m.ninv = 0 - x;
+    m.r1 = (0 - n) % n;
+    return m;
+}
+
+__device__ __forceinline__ uint64_t addmod(uint64_t a, uint64_t b, uint64_t n) {
+    uint64_t s = a + b;
+    if (s < a || s >= n) s -= n;
+    return s;
+}
+
+__device__ __forceinline__ bool mr_witness(uint64_t a, uint64_t d, int s, const Mont& m) {
+    // aR mod n = a * r1 mod n by repeated addition (a <= 37)
+    uint64_t aR = 0;
+    for (uint64_t k = 0; k < a; ++k) aR = addmod(aR, m.r1, m.n);
+    uint64_t x = m.r1;
+    uint64_t base = aR;
+    uint64_t e = d;
+    while (e) {
+        if (e & 1) x = mont_mul(x, base, m);
+        base = mont_mul(base, base, m);
+        e >>= 1;
+    }
+    uint64_t one = m.r1, minus1 = m.n - m.r1;
+    if (x == one || x == minus1) return true;
+    for (int r = 1; r < s; ++r) {
+        x = mont_mul(x, x, m);
+        if (x == minus1) return true;
+    }
+    return false;
+}
+
+__device__ __forceinline__ bool is_prime_u64_dev(uint64_t n) {
+    const uint32_t w[12] = {2, 3, 5, 7, 11, 13, 17, 19, 23, 29, 31, 37};
+    if (n < 41) {
+        for (int i = 0; i < 12; ++i)
+            if (n == w[i]) return true;
+        return false;
+    }
+    for (int i = 0; i < 12; ++i)
+        if (n % w[i] == 0) return false;
+    uint64_t d = n - 1;
+    int s = 0;
+    while ((d & 1) == 0) {
+        d >>= 1;
+        ++s;
+    }
+    Mont m = mont_init(n);
+    for (int i = 0; i < 12; ++i)
+        if (!mr_witness(w[i], d, s, m)) return false;
+    return true;
+}
+
+} // namespace gbk

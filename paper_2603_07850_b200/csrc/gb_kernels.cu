@@ -1,0 +1,724 @@
+// gb_kernels.cu -- sm_100a kernels of the B200 Goldbach verifier.
+//
+//   K1  k_seed_primes / k_sieve_interval / k_count_words / k_scan /
+//       k_compact          base primes <= sqrt_bound on device
+//                          (build_base_primes, sieve.cpp:44-70)
+//   K2+K3 k_verify_blocks  fused segmented sieve (shared-memory bit tile,
+//                          presieve patterns + atomicAnd strikes) and the
+//                          Goldbach minimal-p check over the same tile
+//                          (tiled_sieve_segment sieve.cpp:91-156 +
+//                          phase1_verify verifier.cpp:45-104)
+//       k_segment_offsets  per-segment first-multiple cells of tile primes
+//       k_large_strike     primes > P_TILE_MAX struck into an L2-resident
+//                          segment bitmask (global REDs), ANDed by K2
+//   K4  k_stragglers       Phase 1 continuation past the in-tile halo and
+//                          Phase 2 (phase2_resolve, verifier.cpp:129-165)
+//                          with device Miller-Rabin
+//       k_finalize         per-segment record (verify_segment's report,
+//                          verifier.cpp:167-206, + checksum)
+#include "gb_kernels.h"
+
+#include <algorithm>
+#include <cstdio>
+
+namespace gbk {
+
+// ============================================================ table init
+// Presieve patterns and the reversed Phase 1 prime masks.
+__global__ void k_init_tables(uint32_t* pat, uint64_t* pmr, uint64_t p_small) {
+    const uint32_t gp[4][3] = {{3, 5, 7}, {17, 19, 23}, {29, 31, 37}, {41, 43, 47}};
+    const uint32_t gp1x[2] = {11, 13};
+    uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t nthr = gridDim.x * blockDim.x;
+    for (int g = 0; g < 4; ++g) {
+        uint32_t P = pg_p(g);
+        uint32_t nw = pg_off(g + 1) - pg_off(g);
+        for (uint32_t w = tid; w < nw; w += nthr) {
+            uint32_t v = 0;
+            for (int bit = 0; bit < 32; ++bit) {
+                uint32_t k = (w * 32 + bit) % P;
+                uint32_t q = 2 * k + 1; // odd value represented (mod 2P)
+                bool comp = false;
+                for (int t = 0; t < 3; ++t) comp |= (q % gp[g][t]) == 0;
+                if (g == 0) comp |= (q % gp1x[0]) == 0 || (q % gp1x[1]) == 0;
+                if (!comp) v |= 1u << bit;
+            }
+            pat[pg_off(g) + w] = v;
+        }
+    }
+    // pmr[k] bit (63 - j') set iff p = 3 + 2(64k + j') is prime and <= p_small
+    for (uint32_t k = tid; k < (uint32_t)NWIN; k += nthr) {
+        uint64_t m = 0;
+        for (int jp = 0; jp < 64; ++jp) {
+            uint32_t p = 3 + 2 * (64 * k + jp);
+            bool pr = p <= p_small;
+            for (uint32_t d = 3; pr && d * d <= p; d += 2) pr = (p % d) != 0;
+            if (pr) m |= 1ull << (63 - jp);
+        }
+        pmr[k] = m;
+    }
+}
+
+// ============================================================ K1
+// Odd primes <= lim (lim <= 65536) by one CTA: seeds for the table sieve.
+__global__ void k_seed_primes(uint32_t lim, uint32_t* out, uint32_t* count) {
+    __shared__ uint32_t bits[65536 / 64 + 1]; // bit i <-> 2i+1
+    const uint32_t nb = lim / 2 + 1;
+    for (uint32_t i = threadIdx.x; i < (nb + 31) / 32; i += blockDim.x) bits[i] = ~0u;
+    __syncthreads();
+    for (uint32_t p = 3 + 2 * threadIdx.x; p * p <= lim; p += 2 * blockDim.x) {
+        for (uint32_t m = p * p; m <= lim; m += 2 * p) atomicAnd(&bits[m >> 6], ~(1u << ((m >> 1) & 31)));
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t c = 0;
+        for (uint32_t v = 3; v <= lim; v += 2)
+            if ((bits[v >> 6] >> ((v >> 1) & 31)) & 1) out[c++] = v;
+        *count = c;
+    }
+}
+
+// ------------------------------------------------------------ tile sieve
+// Presieve (patterns), fix-ups and strikes of one W-cell window in shared
+// memory.  OffsetFn(i, p) returns the window cell of the first odd multiple
+// of p >= max(p^2, q_w), or >= W when p does not strike the window.
+struct SmemTables {
+    uint32_t pat[PAT_WORDS];
+};
+
+__device__ __forceinline__ void presieve_window(uint32_t* tile, const uint32_t* pat, uint64_t q_w) {
+    // phase of each group: k0 = ((q_w - 1)/2) mod P
+    uint32_t o[4], step[4];
+    const uint64_t k0 = (q_w - 1) >> 1;
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        uint32_t P = pg_p(g);
+        uint32_t ph = (uint32_t)(k0 % P);
+        o[g] = (uint32_t)((ph + 32ull * threadIdx.x) % P);
+        step[g] = (32u * blockDim.x) % P;
+    }
+    for (uint32_t wd = threadIdx.x; wd < (uint32_t)TILE_WORDS; wd += blockDim.x) {
+        uint32_t v = ~0u;
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const uint32_t* pg = pat + pg_off(g);
+            uint32_t og = o[g];
+            uint32_t lo = pg[og >> 5], hi = pg[(og >> 5) + 1];
+            v &= __funnelshift_r(lo, hi, og & 31);
+            og += step[g];
+            if (og >= pg_p(g)) og -= pg_p(g);
+            o[g] = og;
+        }
+        tile[wd] = v;
+    }
+}
+
+// After presieve: restore the pattern primes themselves and clear q = 1.
+__device__ __forceinline__ void presieve_fixup(uint32_t* tile, uint64_t q_w) {
+    if (threadIdx.x == 0 && q_w <= 47) {
+        if (q_w == 1) atomicAnd(&tile[0], ~1u);
+#pragma unroll
+        for (int t = 0; t < 14; ++t) {
+            uint64_t p = pat_prime(t);
+            if (p >= q_w) {
+                uint64_t c = (p - q_w) >> 1;
+                if (c < W) atomicOr(&tile[c >> 5], 1u << (c & 31));
+            }
+        }
+    }
+}
+
+__device__ __forceinline__ void strike(uint32_t* tile, uint32_t c) {
+    atomicAnd(&tile[c >> 5], ~(1u << (c & 31)));
+}
+
+// warp-cooperative strikes (p < P_WARP_MAX) then thread-per-prime strikes
+template <class OffsetFn>
+__device__ __forceinline__ void strike_primes(uint32_t* tile, const uint32_t* __restrict__ primes,
+                                              uint32_t iA0, uint32_t iA1, uint32_t iB1,
+                                              OffsetFn off_of) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t nwarps = blockDim.x >> 5;
+    for (uint32_t i = iA0 + warp; i < iA1; i += nwarps) {
+        uint32_t p = primes[i];
+        uint32_t off = off_of(i, p, false);
+        if (off >= W) continue;
+        uint32_t c = off + lane * p;
+        const uint32_t step = 32 * p;
+        while (c < W) {
+            strike(tile, c);
+            c += step;
+        }
+    }
+    for (uint32_t i = iA1 + threadIdx.x; i < iB1; i += blockDim.x) {
+        uint32_t p = primes[i];
+        uint32_t c = off_of(i, p, true);
+        while (c < W) {
+            strike(tile, c);
+            c += p;
+        }
+    }
+}
+
+// Generic window offset from a 64-bit window start (K1 / interval sieve).
+struct DirectOffset {
+    uint64_t q_w;
+    __device__ __forceinline__ uint32_t operator()(uint32_t, uint32_t p, bool) const {
+        uint64_t c = first_cell_u64(q_w, p);
+        return c < W ? (uint32_t)c : W;
+    }
+};
+
+// Sieve-only kernel: bits of odd [lo, hi] into out (cell i <-> lo + 2i),
+// cells past hi cleared.  primes: odd primes covering hi (p^2 > hi ignored).
+__global__ void __launch_bounds__(THREADS) k_sieve_interval(uint64_t lo, uint64_t n_cells,
+                                                            const uint32_t* __restrict__ primes,
+                                                            uint32_t iA0, uint32_t iA1, uint32_t iB1,
+                                                            const uint32_t* __restrict__ gpat,
+                                                            uint32_t* __restrict__ out) {
+    extern __shared__ uint32_t smem[];
+    uint32_t* tile = smem;                       // TILE_WORDS + 1
+    uint32_t* pat = smem + TILE_WORDS + 1;       // PAT_WORDS
+    for (uint32_t i = threadIdx.x; i < PAT_WORDS; i += blockDim.x) pat[i] = gpat[i];
+    __syncthreads();
+    const uint64_t nblk = (n_cells + W - 1) / W;
+    for (uint64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
+        const uint64_t q_w = lo + 2 * blk * (uint64_t)W;
+        presieve_window(tile, pat, q_w);
+        __syncthreads();
+        presieve_fixup(tile, q_w);
+        strike_primes(tile, primes, iA0, iA1, iB1, DirectOffset{q_w});
+        __syncthreads();
+        const uint64_t base_word = blk * (W / 32);
+        const uint64_t total_words = (n_cells + 31) / 32;
+        for (uint32_t wd = threadIdx.x; wd < (uint32_t)TILE_WORDS; wd += blockDim.x) {
+            uint64_t gw = base_word + wd;
+            if (gw >= total_words) break;
+            uint32_t v = tile[wd];
+            uint64_t cell0 = gw * 32;
+            if (cell0 + 32 > n_cells) v &= (1u << (n_cells - cell0)) - 1; // n_cells - cell0 < 32
+            out[gw] = v;
+        }
+        __syncthreads();
+    }
+}
+
+__global__ void k_count_words(const uint32_t* __restrict__ bits, uint64_t n_words, uint32_t chunk,
+                              uint32_t* __restrict__ counts) {
+    // counts[c] = popcount of words [c*chunk, (c+1)*chunk)
+    uint64_t c = blockIdx.x;
+    uint64_t w0 = c * chunk, w1 = min((uint64_t)(c + 1) * chunk, n_words);
+    uint32_t s = 0;
+    for (uint64_t w = w0 + threadIdx.x; w < w1; w += blockDim.x) s += __popc(bits[w]);
+    for (int o = 16; o; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    __shared__ uint32_t red[32];
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint32_t t = 0;
+        for (uint32_t i = 0; i < blockDim.x / 32; ++i) t += red[i];
+        counts[c] = t;
+    }
+}
+
+// exclusive scan of n counts (single CTA, serial chunks) -> offsets; total
+__global__ void k_scan(const uint32_t* counts, uint64_t n, uint64_t* offsets, uint64_t* total) {
+    __shared__ uint64_t part[1024];
+    uint64_t per = (n + blockDim.x - 1) / blockDim.x;
+    uint64_t i0 = threadIdx.x * per, i1 = min(i0 + per, n);
+    uint64_t s = 0;
+    for (uint64_t i = i0; i < i1; ++i) s += counts[i];
+    part[threadIdx.x] = s;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        uint64_t run = 0;
+        for (uint32_t t = 0; t < blockDim.x; ++t) {
+            uint64_t v = part[t];
+            part[t] = run;
+            run += v;
+        }
+        *total = run;
+    }
+    __syncthreads();
+    uint64_t run = part[threadIdx.x];
+    for (uint64_t i = i0; i < i1; ++i) {
+        offsets[i] = run;
+        run += counts[i];
+    }
+}
+
+// primes[offset..] = lo + 2*(bit index) for each set bit, in order.
+__global__ void k_compact(const uint32_t* __restrict__ bits, uint64_t n_words, uint32_t chunk,
+                          const uint64_t* __restrict__ offsets, uint64_t lo, uint32_t* __restrict__ primes) {
+    uint64_t c = blockIdx.x;
+    uint64_t w0 = c * chunk, w1 = min((uint64_t)(c + 1) * chunk, n_words);
+    __shared__ uint32_t wsum[33];
+    uint64_t base = offsets[c];
+    // process the chunk in rounds of blockDim.x words, preserving order
+    for (uint64_t r0 = w0; r0 < w1; r0 += blockDim.x) {
+        uint64_t w = r0 + threadIdx.x;
+        uint32_t v = w < w1 ? bits[w] : 0;
+        uint32_t cnt = __popc(v);
+        // block exclusive scan of cnt
+        uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+        uint32_t x = cnt;
+        for (int o = 1; o < 32; o <<= 1) {
+            uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= (uint32_t)o) x += y;
+        }
+        if (lane == 31) wsum[warp] = x;
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint32_t run = 0;
+            for (uint32_t k = 0; k < blockDim.x / 32; ++k) {
+                uint32_t t = wsum[k];
+                wsum[k] = run;
+                run += t;
+            }
+            wsum[32] = run;
+        }
+        __syncthreads();
+        uint64_t pos = base + wsum[warp] + (x - cnt);
+        while (v) {
+            uint32_t bit = __ffs(v) - 1;
+            v &= v - 1;
+            primes[pos++] = (uint32_t)(lo + 2 * (w * 32 + bit));
+        }
+        base += wsum[32];
+        __syncthreads();
+    }
+}
+
+// ============================================================ segment setup
+// c0[s*np + i] = cell (relative to the slot's qbase) of the first odd
+// multiple of tile prime i (index iA0 + i) >= max(p^2, qbase); ~0 if >= 2^32.
+__global__ void k_segment_offsets(const SegJob* __restrict__ jobs, uint32_t nslots,
+                                  const uint32_t* __restrict__ primes, uint32_t iA0, uint32_t np,
+                                  uint32_t* __restrict__ c0) {
+    uint64_t total = (uint64_t)nslots * np;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t s = (uint32_t)(t / np), i = (uint32_t)(t % np);
+        uint64_t c = first_cell_u64(jobs[s].qbase, primes[iA0 + i]);
+        c0[t] = c >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c;
+    }
+}
+
+// Primes above P_TILE_MAX: strike the slot's global bitmask (cells relative
+// to qbase) with RED.AND; K2 ANDs the words into its tile.
+__global__ void k_large_strike(const SegJob* __restrict__ jobs, uint32_t nslots,
+                               const uint32_t* __restrict__ primes, uint64_t iL0, uint64_t iL1,
+                               uint32_t* __restrict__ qg, uint64_t qg_stride_words) {
+    uint64_t np = iL1 - iL0;
+    uint64_t total = np * nslots;
+    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
+         t += (uint64_t)gridDim.x * blockDim.x) {
+        uint32_t s = (uint32_t)(t / np);
+        uint64_t i = iL0 + t % np;
+        const SegJob& j = jobs[s];
+        uint64_t ncells = (uint64_t)j.qg_words * 32;
+        uint64_t p = primes[i];
+        uint64_t c = first_cell_u64(j.qbase, p);
+        uint32_t* g = qg + s * qg_stride_words;
+        for (; c < ncells; c += p) atomicAnd(&g[c >> 5], ~(1u << (c & 31)));
+    }
+}
+
+// ============================================================ K2 + K3
+// Offsets for the verify path from the per-segment c0 table.
+struct SegOffset {
+    const uint32_t* c0;  // this slot's c0 row (index i - iA0)
+    uint32_t iA0;
+    uint32_t B;          // block start cell relative to qbase
+    bool low;            // window starts at q = 1
+    __device__ __forceinline__ uint32_t operator()(uint32_t i, uint32_t p, bool fp) const {
+        if (low) {
+            uint64_t pp = (uint64_t)p * p;
+            uint64_t c = (pp - 1) >> 1;
+            return c < W ? (uint32_t)c : W;
+        }
+        uint32_t c = c0[i - iA0];
+        if (c >= B) {
+            uint32_t d = c - B;
+            return d < W ? d : W;
+        }
+        uint32_t x = B - c;
+        uint32_t r = fp ? mod_fp(x, p, __frcp_rn((float)p)) : x % p;
+        return r ? p - r : 0;
+    }
+};
+
+
+
+__device__ __forceinline__ uint64_t window_bits(const uint32_t* tile, int64_t x) {
+    // 64 cells [x-64, x) as a u64 (bit 63 <-> cell x-1); cells < 0 read as 0
+    if (x >= 64) {
+        uint32_t lo = (uint32_t)(x - 64);
+        uint32_t wi = lo >> 5, s = lo & 31;
+        uint32_t w0 = tile[wi], w1 = tile[wi + 1], w2 = tile[wi + 2];
+        uint32_t l32 = __funnelshift_r(w0, w1, s);
+        uint32_t h32 = __funnelshift_r(w1, w2, s);
+        return ((uint64_t)h32 << 32) | l32;
+    }
+    if (x <= 0) return 0;
+    uint64_t v = ((uint64_t)tile[1] << 32) | tile[0];
+    return v << (64 - x);
+}
+
+__global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
+    extern __shared__ uint32_t smem[];
+    uint32_t* tile = smem;                                  // TILE_WORDS + 3 (pad)
+    uint32_t* pat = smem + TILE_WORDS + 3;                  // PAT_WORDS
+    uint64_t* pmr = (uint64_t*)(pat + PAT_WORDS + (PAT_WORDS & 1)); // NWIN
+    __shared__ uint32_t s_blk;
+    __shared__ unsigned long long s_red[NWARPS][3];
+
+    for (uint32_t i = threadIdx.x; i < PAT_WORDS; i += blockDim.x) pat[i] = A.gpat[i];
+    for (uint32_t i = threadIdx.x; i < (uint32_t)NWIN; i += blockDim.x) pmr[i] = A.pmr[i];
+    for (uint32_t i = threadIdx.x; i < 3; i += blockDim.x) tile[TILE_WORDS + i] = 0;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t jlim_small = A.p_small >= 3 ? (uint32_t)min((A.p_small - 3) / 2, (uint64_t)0xFFFFFFFFu) : 0;
+
+    for (;;) {
+        __syncthreads();
+        if (threadIdx.x == 0) s_blk = atomicAdd(A.block_counter, 1u);
+        __syncthreads();
+        const uint32_t fb = s_blk;
+        if (fb >= A.total_blocks) break;
+        // locate slot (few slots: linear scan)
+        uint32_t s = 0;
+        while (s + 1 < A.nslots && A.jobs[s + 1].block_prefix <= fb) ++s;
+        const SegJob J = A.jobs[s];
+        const uint32_t b = fb - J.block_prefix;
+        const bool low = b < J.b1;
+        const uint64_t q_w = low ? 1ull : J.qbase + 2ull * (uint64_t)(b - J.b1) * E;
+        const uint32_t B = low ? 0u : (b - J.b1) * E;
+
+        // ---- K2: sieve the window
+        presieve_window(tile, pat, q_w);
+        __syncthreads();
+        presieve_fixup(tile, q_w);
+        SegOffset off{A.c0 + (uint64_t)s * A.np, A.iA0, B, low};
+        strike_primes(tile, A.primes, A.iA0, A.iA1, A.iB1, off);
+        __syncthreads();
+        if (A.qg != nullptr && !low && J.qg_words) {
+            const uint32_t* g = A.qg + s * A.qg_stride_words + B / 32;
+            uint32_t lim = min((uint32_t)TILE_WORDS, J.qg_words - B / 32);
+            for (uint32_t wd = threadIdx.x; wd < lim; wd += blockDim.x) tile[wd] &= __ldg(g + wd);
+            __syncthreads();
+        }
+
+        // ---- K3: minimal p per even, while the tile is in shared memory
+        const uint32_t i0 = b * E;
+        const uint32_t ne = min(E, J.evens - i0);
+        // top cell of the block's first even: n - 3 - q_w over 2
+        const uint32_t t0 = low ? (uint32_t)((J.a - 4) >> 1) : (uint32_t)JH;
+        uint64_t sp = 0, spi = 0, key = 0;
+        for (uint32_t base = warp * 32; base < ne; base += blockDim.x) {
+            const uint32_t il = base + lane;
+            if (il < ne) {
+                const uint32_t iseg = i0 + il;
+                const uint64_t n = J.a + 2ull * iseg;
+                uint64_t p = 0;
+                if (n == 4) {
+                    p = 2;
+                } else {
+                    const int64_t t = (int64_t)t0 + il;
+                    // candidates j <= jmax: p <= p_small, q >= 3, in-tile
+                    const uint64_t jq = (n - 6) >> 1;
+                    uint32_t jmax = jlim_small;
+                    if (jq < jmax) jmax = (uint32_t)jq;
+                    const uint32_t kmax = min((uint32_t)NWIN, jmax / 64 + 1);
+                    uint32_t k = 0;
+                    for (; k < kmax; ++k) {
+                        uint64_t m = window_bits(tile, t + 1 - 64 * (int64_t)k) & pmr[k];
+                        if (m) {
+                            p = 3 + 2 * (64ull * k + __clzll(m));
+                            break;
+                        }
+                    }
+                    // a hit beyond jmax cannot occur: pmr caps p_small and
+                    // cells below q = 3 are zero (low window) or absent
+                    if (!p) {
+                        bool more = (uint64_t)JH <= jmax; // candidates beyond the halo remain
+                        uint32_t flags = more ? F_NEED_P1 : F_P1_FAIL;
+                        if (n == A.inject) flags |= F_INJECT;
+                        unsigned idx = atomicAdd(A.list_count, 1u);
+                        if (idx < A.list_cap) A.list[idx] = StragEntry{s, iseg, (uint32_t)JH, flags};
+                    }
+                }
+                if (p) {
+                    sp += p;
+                    spi += p * (uint64_t)iseg;
+                    uint64_t kk = (p << 32) | (0xFFFFFFFFu - iseg);
+                    key = kk > key ? kk : key;
+                    if (n == A.inject) {
+                        unsigned idx = atomicAdd(A.list_count, 1u);
+                        if (idx < A.list_cap) A.list[idx] = StragEntry{s, iseg, 0u, F_INJECT | F_OBSERVED};
+                    }
+                }
+                if (A.pmin_out) A.pmin_out[iseg] = p;
+            }
+        }
+        // ---- block reduction -> slot accumulators
+        for (int o = 16; o; o >>= 1) {
+            sp += __shfl_xor_sync(0xffffffffu, sp, o);
+            spi += __shfl_xor_sync(0xffffffffu, spi, o);
+            uint64_t ok = __shfl_xor_sync(0xffffffffu, key, o);
+            key = ok > key ? ok : key;
+        }
+        if (lane == 0) {
+            s_red[warp][0] = sp;
+            s_red[warp][1] = spi;
+            s_red[warp][2] = key;
+        }
+        __syncthreads();
+        if (threadIdx.x == 0) {
+            uint64_t S = 0, SPI = 0, K = 0;
+            for (int w = 0; w < NWARPS; ++w) {
+                S += s_red[w][0];
+                SPI += s_red[w][1];
+                K = s_red[w][2] > K ? s_red[w][2] : K;
+            }
+            atomicAdd(&A.acc[s].sum, (unsigned long long)S);
+            atomicAdd(&A.acc[s].hash, (unsigned long long)((J.a >> 1) * S + SPI));
+            if (K) atomicMax(&A.acc[s].key, (unsigned long long)K);
+        }
+    }
+}
+
+// ============================================================ K4
+// One CTA per straggler entry: ascending candidate scan in rounds of
+// blockDim.x odd p; the smallest hit of the first round with a hit wins.
+__device__ uint64_t scan_min_prime(uint64_t n, uint64_t p_first, uint64_t p_last) {
+    // smallest odd prime p in [p_first, p_last] with n - p prime; 0 if none
+    __shared__ unsigned long long s_best;
+    if ((p_first & 1) == 0) ++p_first;
+    for (uint64_t r0 = p_first; r0 <= p_last; r0 += 2ull * blockDim.x) {
+        if (threadIdx.x == 0) s_best = ~0ull;
+        __syncthreads();
+        uint64_t p = r0 + 2ull * threadIdx.x;
+        if (p <= p_last && p >= r0 && is_prime_u64_dev(p) && is_prime_u64_dev(n - p))
+            atomicMin(&s_best, (unsigned long long)p);
+        __syncthreads();
+        uint64_t best = s_best;
+        __syncthreads();
+        if (best != ~0ull) return best;
+        if (r0 > ~0ull - 2ull * blockDim.x) break; // no wrap
+    }
+    return 0;
+}
+
+__global__ void k_stragglers(const SegJob* __restrict__ jobs, const StragEntry* __restrict__ list,
+                             const unsigned int* __restrict__ list_count, uint32_t list_cap,
+                             uint64_t p_small, StragResult* __restrict__ res,
+                             uint64_t* pmin_out) {
+    uint32_t cnt = min(*list_count, list_cap);
+    for (uint32_t e = blockIdx.x; e < cnt; e += gridDim.x) {
+        StragEntry en = list[e];
+        const SegJob& J = jobs[en.slot];
+        uint64_t n = J.a + 2ull * en.i_seg;
+        uint64_t p1 = 0, p2 = 0;
+        bool p1_failed = (en.flags & F_P1_FAIL) != 0;
+        if (en.flags & F_NEED_P1) {
+            // Phase 1 continuation: odd primes p in [3 + 2*j_next, min(p_small, n-3)]
+            uint64_t pf = 3 + 2ull * en.j_next;
+            uint64_t pl = min(p_small, n - 3);
+            if (pf <= pl) p1 = scan_min_prime(n, pf, pl);
+            p1_failed = p1 == 0;
+        }
+        if (p1_failed && !(en.flags & F_INJECT)) {
+            // Phase 2: every prime <= min(p_small, n-3) failed (and p = 2 only
+            // works for n = 4), so continue with primes > p_small, p <= n/2
+            uint64_t pf = p_small + 1;
+            uint64_t pl = n / 2;
+            if (pf <= pl) p2 = scan_min_prime(n, pf, pl);
+        }
+        if (threadIdx.x == 0) {
+            res[e] = StragResult{p1, p2};
+            if (pmin_out && p1) pmin_out[en.i_seg] = p1;
+        }
+    }
+}
+
+// Standalone phase2_resolve (verifier.cpp:129-165) for one n.
+__global__ void k_phase2_one(uint64_t n, uint64_t* out) {
+    uint64_t half = n / 2;
+    __shared__ uint64_t s_p;
+    if (threadIdx.x == 0) s_p = (2 <= half && is_prime_u64_dev(n - 2)) ? 2 : 0;
+    __syncthreads();
+    uint64_t r = s_p;
+    if (r == 0 && half >= 3) r = scan_min_prime(n, 3, half);
+    if (threadIdx.x == 0) *out = r;
+}
+
+__global__ void k_is_prime_batch(const uint64_t* __restrict__ v, uint8_t* __restrict__ out, uint64_t n) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        out[i] = is_prime_u64_dev(v[i]) ? 1 : 0;
+}
+
+// ============================================================ finalize
+// One thread: merge tile accumulators and straggler results into records.
+__device__ void observe(DevRecord& r, uint64_t p, uint64_t n) {
+    r.pmin_sum += p;
+    r.pmin_hash += p * (n >> 1);
+    if (p > r.max_p || (p == r.max_p && r.max_p != 0 && n < r.max_n)) {
+        r.max_p = p;
+        r.max_n = n;
+    }
+}
+
+__device__ void add_ce(DevRecord& r, uint64_t n) {
+    // keep the smallest GB_REC_MAX_CE ascending
+    uint64_t k = r.n_ce < GB_REC_MAX_CE ? r.n_ce : GB_REC_MAX_CE;
+    while (k > 0 && r.ce[k - 1] > n) {
+        if (k < GB_REC_MAX_CE) r.ce[k] = r.ce[k - 1];
+        --k;
+    }
+    if (k < GB_REC_MAX_CE) r.ce[k] = n;
+    r.n_ce++;
+}
+
+__global__ void k_finalize(const SegJob* __restrict__ jobs, uint32_t nslots, const SlotAcc* __restrict__ acc,
+                           const StragEntry* __restrict__ list, const unsigned int* __restrict__ list_count,
+                           uint32_t list_cap, const StragResult* __restrict__ res, DevRecord* __restrict__ out) {
+    if (threadIdx.x != 0 || blockIdx.x != 0) return;
+    uint32_t cnt = *list_count;
+    for (uint32_t s = 0; s < nslots; ++s) {
+        DevRecord r{};
+        const SegJob& J = jobs[s];
+        r.a = J.a;
+        r.b = J.b;
+        r.evens = J.evens;
+        r.pmin_sum = acc[s].sum;
+        r.pmin_hash = acc[s].hash;
+        if (acc[s].key) {
+            uint64_t k = acc[s].key;
+            r.max_p = k >> 32;
+            r.max_n = J.a + 2ull * (0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFu));
+        }
+        r.overflow = cnt > list_cap;
+        out[s] = r;
+    }
+    uint32_t m = min(cnt, list_cap);
+    for (uint32_t e = 0; e < m; ++e) {
+        StragEntry en = list[e];
+        DevRecord& r = out[en.slot];
+        uint64_t n = jobs[en.slot].a + 2ull * en.i_seg;
+        if (en.flags & F_OBSERVED) { // injected, Phase 1 certified in-tile
+            r.unverified++;
+            add_ce(r, n);
+            continue;
+        }
+        uint64_t p1 = res[e].p1, p2 = res[e].p2;
+        if (p1) observe(r, p1, n);
+        if (en.flags & F_INJECT) {
+            r.unverified++;
+            add_ce(r, n);
+            continue;
+        }
+        if (p1) continue;
+        r.unverified++;
+        if (p2) {
+            r.phase2++;
+            observe(r, p2, n);
+        } else {
+            add_ce(r, n);
+        }
+    }
+}
+
+// ============================================================ launchers
+cudaError_t launch_init_tables(uint32_t* pat, uint64_t* pmr, uint64_t p_small, cudaStream_t st) {
+    k_init_tables<<<64, 256, 0, st>>>(pat, pmr, p_small);
+    return cudaGetLastError();
+}
+cudaError_t launch_seed_primes(uint32_t lim, uint32_t* out, uint32_t* count, cudaStream_t st) {
+    k_seed_primes<<<1, 1024, 0, st>>>(lim, out, count);
+    return cudaGetLastError();
+}
+cudaError_t launch_sieve_interval(uint64_t lo, uint64_t n_cells, const uint32_t* primes, uint32_t iA0,
+                                  uint32_t iA1, uint32_t iB1, const uint32_t* pat, uint32_t* out,
+                                  int grid, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_sieve_interval, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)SIEVE_SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_sieve_interval<<<grid, THREADS, SIEVE_SMEM, st>>>(lo, n_cells, primes, iA0, iA1, iB1, pat, out);
+    return cudaGetLastError();
+}
+cudaError_t launch_count_words(const uint32_t* bits, uint64_t n_words, uint32_t chunk, uint32_t* counts,
+                               uint64_t n_chunks, cudaStream_t st) {
+    k_count_words<<<(unsigned)n_chunks, 256, 0, st>>>(bits, n_words, chunk, counts);
+    return cudaGetLastError();
+}
+cudaError_t launch_scan(const uint32_t* counts, uint64_t n, uint64_t* offsets, uint64_t* total,
+                        cudaStream_t st) {
+    k_scan<<<1, 1024, 0, st>>>(counts, n, offsets, total);
+    return cudaGetLastError();
+}
+cudaError_t launch_compact(const uint32_t* bits, uint64_t n_words, uint32_t chunk, const uint64_t* offsets,
+                           uint64_t lo, uint32_t* primes, uint64_t n_chunks, cudaStream_t st) {
+    k_compact<<<(unsigned)n_chunks, 256, 0, st>>>(bits, n_words, chunk, offsets, lo, primes);
+    return cudaGetLastError();
+}
+cudaError_t launch_segment_offsets(const SegJob* jobs, uint32_t nslots, const uint32_t* primes,
+                                   uint32_t iA0, uint32_t np, uint32_t* c0, cudaStream_t st) {
+    uint64_t total = (uint64_t)nslots * np;
+    if (!total) return cudaSuccess;
+    unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
+    k_segment_offsets<<<grid, 256, 0, st>>>(jobs, nslots, primes, iA0, np, c0);
+    return cudaGetLastError();
+}
+cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, uint64_t iL0,
+                                uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, cudaStream_t st) {
+    uint64_t total = (uint64_t)nslots * (iL1 - iL0);
+    if (!total) return cudaSuccess;
+    unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 32);
+    k_large_strike<<<grid, 256, 0, st>>>(jobs, nslots, primes, iL0, iL1, qg, qg_stride_words);
+    return cudaGetLastError();
+}
+cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaError_t e = cudaFuncSetAttribute(k_verify_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)VERIFY_SMEM);
+        if (e != cudaSuccess) return e;
+        attr = true;
+    }
+    k_verify_blocks<<<grid, THREADS, VERIFY_SMEM, st>>>(a);
+    return cudaGetLastError();
+}
+cudaError_t launch_stragglers(const SegJob* jobs, const StragEntry* list, const unsigned int* list_count,
+                              uint32_t list_cap, uint64_t p_small, StragResult* res, uint64_t* pmin_out,
+                              int grid, cudaStream_t st) {
+    k_stragglers<<<grid, 128, 0, st>>>(jobs, list, list_count, list_cap, p_small, res, pmin_out);
+    return cudaGetLastError();
+}
+cudaError_t launch_finalize(const SegJob* jobs, uint32_t nslots, const SlotAcc* acc, const StragEntry* list,
+                            const unsigned int* list_count, uint32_t list_cap, const StragResult* res,
+                            DevRecord* out, cudaStream_t st) {
+    k_finalize<<<1, 32, 0, st>>>(jobs, nslots, acc, list, list_count, list_cap, res, out);
+    return cudaGetLastError();
+}
+cudaError_t launch_phase2_one(uint64_t n, uint64_t* out, cudaStream_t st) {
+    k_phase2_one<<<1, 128, 0, st>>>(n, out);
+    return cudaGetLastError();
+}
+cudaError_t launch_is_prime_batch(const uint64_t* v, uint8_t* out, uint64_t n, cudaStream_t st) {
+    if (!n) return cudaSuccess;
+    unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 8);
+    k_is_prime_batch<<<grid, 256, 0, st>>>(v, out, n);
+    return cudaGetLastError();
+}
+int verify_occupancy(int* blocks_per_sm) {
+    cudaFuncSetAttribute(k_verify_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)VERIFY_SMEM);
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_verify_blocks, THREADS,
+                                                              VERIFY_SMEM);
+}
+
+} // namespace gbk
