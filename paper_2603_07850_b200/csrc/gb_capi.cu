@@ -1,0 +1,749 @@
+// gb_capi.cu -- implementation of the C-ABI boundary (include/goldbach_b200.h).
+//
+// One gb_dev per GPU.  Segments submitted by the host worker are cut into
+// device pieces (<= 2^31 evens), packed S per batch, and each batch runs
+// as one stream of kernels:
+//   H2D jobs -> [large-prime strike] -> segment offsets -> fused sieve+check
+//   -> stragglers/Phase 2 -> finalize -> D2H records
+// Up to NBATCH batches are in flight on separate streams so the tail of one
+// fused launch overlaps the head of the next.  Nothing here computes on the
+// CPU: host code only schedules, copies records and merges them
+// (MinPrimeMax / sums / counterexample lists, pool.cpp:159-174 semantics).
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <deque>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "gb_kernels.h"
+
+using namespace gbk;
+
+namespace {
+
+constexpr int NBATCH = 3;                 // batches in flight per device
+constexpr uint32_t SLOTS = 8;             // pieces per batch
+constexpr uint32_t LIST_CAP = 1u << 20;   // straggler entries per batch
+constexpr uint64_t MAX_PIECE = 1ull << 31;
+
+thread_local std::string t_err;
+
+double now_s() {
+    return std::chrono::duration<double>(std::chrono::steady_clock::now().time_since_epoch()).count();
+}
+
+uint64_t sqrt_bound_of(uint64_t cover) {
+    // build_base_primes' s (sieve.cpp:48-52): minimal s with s >= cover / s
+    uint64_t s = (uint64_t)std::sqrt((long double)cover);
+    if (s == 0) s = 1;
+    while (s > 1 && (s - 1) >= cover / (s - 1)) --s;
+    while (s < cover / s) ++s;
+    return s;
+}
+
+uint64_t isqrt_floor(uint64_t x) {
+    uint64_t r = (uint64_t)std::sqrt((long double)x);
+    while (r > 0 && r > x / r) --r;
+    while ((r + 1) <= x / (r + 1)) ++r;
+    return r;
+}
+
+struct Piece {
+    uint64_t seq; // user segment sequence number
+    uint64_t a, b;
+};
+
+struct Batch {
+    cudaStream_t st = nullptr;
+    SegJob* d_jobs = nullptr;
+    uint32_t* d_c0 = nullptr;
+    uint32_t* d_qg = nullptr;
+    SlotAcc* d_acc = nullptr;
+    StragEntry* d_list = nullptr;
+    unsigned int* d_counters = nullptr; // [0] block counter, [1] list count
+    StragResult* d_res = nullptr;
+    DevRecord* d_rec = nullptr;
+    SegJob* h_jobs = nullptr;
+    DevRecord* h_rec = nullptr;
+    cudaEvent_t ev_done = nullptr, ev_k0 = nullptr, ev_k1 = nullptr, ev_l0 = nullptr, ev_s1 = nullptr;
+    std::vector<Piece> pieces;
+    bool launched = false;
+    bool timed = false;
+    bool large = false;
+};
+
+struct UserSeg {
+    uint64_t seq, a, b, tag;
+    uint32_t pieces_total = 0, pieces_done = 0;
+    gb_seg_record rec{};
+    double t0 = 0;
+};
+
+} // namespace
+
+struct gb_dev {
+    int device = 0;
+    gb_params prm{};
+    std::string err;
+    int sms = 148, occ = 2;
+    uint64_t sqrt_bound = 0, n_primes = 0;
+    uint32_t* d_primes = nullptr;
+    uint32_t iA0 = 0, iA1 = 0, iB1 = 0; // tile prime index ranges
+    uint64_t iL0 = 0, iL1 = 0;          // large primes
+    uint32_t* d_pat = nullptr;
+    uint64_t* d_pmr = nullptr;
+    uint64_t max_piece = 0;
+    uint64_t qg_stride = 0; // words per slot
+    Batch batches[NBATCH];
+    int fill = -1;                 // batch being filled
+    std::deque<int> inflight;      // launched batches, oldest first
+    std::deque<UserSeg> segs;      // submitted user segments, FIFO
+    uint64_t next_seq = 0;
+    uint64_t launches = 0;
+    bool timing = false;
+    double kms[4] = {0, 0, 0, 0};
+    uint64_t kl[4] = {0, 0, 0, 0};
+    Batch sync;                    // private batch for the synchronous helpers
+};
+
+#define GB_FAIL(dev, code, msg)                      \
+    do {                                             \
+        set_err(dev, msg);                           \
+        return code;                                 \
+    } while (0)
+
+#define CU(dev, expr)                                                                      \
+    do {                                                                                   \
+        cudaError_t _e = (expr);                                                           \
+        if (_e != cudaSuccess) {                                                           \
+            set_err(dev, std::string(#expr) + ": " + cudaGetErrorString(_e));              \
+            return GB_ERR_CUDA;                                                            \
+        }                                                                                  \
+    } while (0)
+
+static void set_err(gb_dev* d, const std::string& m) {
+    if (d) d->err = m;
+    t_err = m;
+}
+
+// --------------------------------------------------------------- batches
+static int batch_alloc(gb_dev* d, Batch& b, bool with_qg) {
+    if (!b.st) CU(d, cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking));
+    uint32_t np = d->iB1 - d->iA0;
+    CU(d, cudaMalloc(&b.d_jobs, SLOTS * sizeof(SegJob)));
+    CU(d, cudaMalloc(&b.d_c0, (size_t)SLOTS * std::max<uint32_t>(np, 1) * 4));
+    if (with_qg && d->iL1 > d->iL0) CU(d, cudaMalloc(&b.d_qg, (size_t)SLOTS * d->qg_stride * 4));
+    CU(d, cudaMalloc(&b.d_acc, SLOTS * sizeof(SlotAcc)));
+    CU(d, cudaMalloc(&b.d_list, (size_t)LIST_CAP * sizeof(StragEntry)));
+    CU(d, cudaMalloc(&b.d_counters, 4 * sizeof(unsigned int)));
+    CU(d, cudaMalloc(&b.d_res, (size_t)LIST_CAP * sizeof(StragResult)));
+    CU(d, cudaMalloc(&b.d_rec, SLOTS * sizeof(DevRecord)));
+    CU(d, cudaMallocHost(&b.h_jobs, SLOTS * sizeof(SegJob)));
+    CU(d, cudaMallocHost(&b.h_rec, SLOTS * sizeof(DevRecord)));
+    CU(d, cudaEventCreateWithFlags(&b.ev_done, cudaEventDisableTiming));
+    CU(d, cudaEventCreate(&b.ev_k0));
+    CU(d, cudaEventCreate(&b.ev_k1));
+    CU(d, cudaEventCreate(&b.ev_l0));
+    CU(d, cudaEventCreate(&b.ev_s1));
+    return GB_OK;
+}
+
+static void batch_free(Batch& b) {
+    cudaFree(b.d_jobs);
+    cudaFree(b.d_c0);
+    cudaFree(b.d_qg);
+    cudaFree(b.d_acc);
+    cudaFree(b.d_list);
+    cudaFree(b.d_counters);
+    cudaFree(b.d_res);
+    cudaFree(b.d_rec);
+    cudaFreeHost(b.h_jobs);
+    cudaFreeHost(b.h_rec);
+    if (b.ev_done) cudaEventDestroy(b.ev_done);
+    if (b.ev_k0) cudaEventDestroy(b.ev_k0);
+    if (b.ev_k1) cudaEventDestroy(b.ev_k1);
+    if (b.ev_l0) cudaEventDestroy(b.ev_l0);
+    if (b.ev_s1) cudaEventDestroy(b.ev_s1);
+    if (b.st) cudaStreamDestroy(b.st);
+    b = Batch{};
+}
+
+// Fill the job descriptor of one piece.
+static void make_job(gb_dev* d, const Piece& pc, SegJob& j, uint32_t prefix) {
+    j.a = pc.a;
+    j.b = pc.b;
+    j.evens = (uint32_t)(((pc.b - pc.a) >> 1) + 1);
+    j.nblocks = (j.evens + E - 1) / E;
+    j.block_prefix = prefix;
+    bool low = (pc.a - 3) < 2ull * JH;
+    j.b1 = low ? 1 : 0;
+    // q of cell 0 of block b1: a - 3 - 2JH + 2*b1*E (>= 3 in both cases)
+    j.qbase = (pc.a - 3 + 2ull * j.b1 * E) - 2ull * JH;
+    uint64_t cells = (uint64_t)j.nblocks * E + JH;
+    j.qg_words = (!low && d->iL1 > d->iL0) ? (uint32_t)((cells + 31) / 32) : 0;
+    j.pad = 0;
+}
+
+static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
+    const uint32_t n = (uint32_t)b.pieces.size();
+    uint32_t prefix = 0;
+    bool large = false;
+    for (uint32_t s = 0; s < n; ++s) {
+        make_job(d, b.pieces[s], b.h_jobs[s], prefix);
+        prefix += b.h_jobs[s].nblocks;
+        large |= b.h_jobs[s].qg_words != 0;
+    }
+    b.large = large;
+    cudaStream_t st = b.st;
+    CU(d, cudaMemcpyAsync(b.d_jobs, b.h_jobs, n * sizeof(SegJob), cudaMemcpyHostToDevice, st));
+    CU(d, cudaMemsetAsync(b.d_acc, 0, n * sizeof(SlotAcc), st));
+    CU(d, cudaMemsetAsync(b.d_counters, 0, 4 * sizeof(unsigned int), st));
+    b.timed = d->timing;
+    if (b.timed) CU(d, cudaEventRecord(b.ev_l0, st));
+    if (large) {
+        CU(d, cudaMemsetAsync(b.d_qg, 0xFF, (size_t)n * d->qg_stride * 4, st));
+        CU(d, launch_large_strike(b.d_jobs, n, d->d_primes, d->iL0, d->iL1, b.d_qg, d->qg_stride, st));
+        d->launches++;
+    }
+    const uint32_t np = d->iB1 - d->iA0;
+    if (np) {
+        CU(d, launch_segment_offsets(b.d_jobs, n, d->d_primes, d->iA0, np, b.d_c0, st));
+        d->launches++;
+    }
+    VerifyArgs A{};
+    A.jobs = b.d_jobs;
+    A.nslots = n;
+    A.total_blocks = prefix;
+    A.primes = d->d_primes;
+    A.iA0 = d->iA0;
+    A.iA1 = d->iA1;
+    A.iB1 = d->iB1;
+    A.np = np;
+    A.c0 = b.d_c0;
+    A.qg = large ? b.d_qg : nullptr;
+    A.qg_stride_words = d->qg_stride;
+    A.gpat = d->d_pat;
+    A.pmr = d->d_pmr;
+    A.p_small = d->prm.p_small;
+    A.inject = d->prm.inject_fail;
+    A.block_counter = b.d_counters;
+    A.acc = b.d_acc;
+    A.list = b.d_list;
+    A.list_count = b.d_counters + 1;
+    A.list_cap = LIST_CAP;
+    A.pmin_out = pmin_out;
+    int grid = std::min<int>(d->sms * d->occ, (int)prefix);
+    if (grid < 1) grid = 1;
+    if (b.timed) CU(d, cudaEventRecord(b.ev_k0, st));
+    CU(d, launch_verify_blocks(A, grid, st));
+    if (b.timed) CU(d, cudaEventRecord(b.ev_k1, st));
+    CU(d, launch_stragglers(b.d_jobs, b.d_list, b.d_counters + 1, LIST_CAP, d->prm.p_small, b.d_res, pmin_out,
+                            d->sms, st));
+    CU(d, launch_finalize(b.d_jobs, n, b.d_acc, b.d_list, b.d_counters + 1, LIST_CAP, b.d_res, b.d_rec, st));
+    if (b.timed) CU(d, cudaEventRecord(b.ev_s1, st));
+    d->launches += 3;
+    CU(d, cudaMemcpyAsync(b.h_rec, b.d_rec, n * sizeof(DevRecord), cudaMemcpyDeviceToHost, st));
+    CU(d, cudaEventRecord(b.ev_done, st));
+    b.launched = true;
+    return GB_OK;
+}
+
+static void rec_merge(gb_seg_record& t, const DevRecord& r) {
+    t.evens_checked += r.evens;
+    t.unverified_p1 += r.unverified;
+    t.phase2_resolved += r.phase2;
+    t.pmin_sum += r.pmin_sum;
+    t.pmin_hash += r.pmin_hash;
+    if (r.max_p != 0 && (r.max_p > t.max_p || (r.max_p == t.max_p && r.max_n < t.max_n))) {
+        t.max_p = r.max_p;
+        t.max_n = r.max_n;
+    }
+    uint64_t stored = std::min<uint64_t>(r.n_ce, GB_REC_MAX_CE);
+    for (uint64_t i = 0; i < stored; ++i) {
+        uint64_t v = r.ce[i];
+        uint64_t k = std::min<uint64_t>(t.n_counterexamples, GB_REC_MAX_CE);
+        while (k > 0 && t.counterexamples[k - 1] > v) {
+            if (k < GB_REC_MAX_CE) t.counterexamples[k] = t.counterexamples[k - 1];
+            --k;
+        }
+        if (k < GB_REC_MAX_CE) t.counterexamples[k] = v;
+        t.n_counterexamples++;
+    }
+    t.n_counterexamples += r.n_ce - stored;
+}
+
+static UserSeg* find_seg(gb_dev* d, uint64_t seq) {
+    for (auto& u : d->segs)
+        if (u.seq == seq) return &u;
+    return nullptr;
+}
+
+// Run pieces one at a time on the private batch and return the merged record
+// (used for the straggler-list overflow fallback and the parity hooks).
+static int run_piece_sync(gb_dev* d, uint64_t a, uint64_t b, DevRecord* out, uint64_t* pmin_out) {
+    Batch& s = d->sync;
+    s.pieces.assign(1, Piece{0, a, b});
+    int rc = batch_launch(d, s, pmin_out);
+    if (rc) return rc;
+    CU(d, cudaEventSynchronize(s.ev_done));
+    CU(d, cudaGetLastError());
+    *out = s.h_rec[0];
+    s.launched = false;
+    return GB_OK;
+}
+
+static int rerun_split(gb_dev* d, uint64_t a, uint64_t b, gb_seg_record& into) {
+    // every straggler entry is one even, so pieces of <= LIST_CAP evens can
+    // never overflow the list
+    const uint64_t span = 2ull * (LIST_CAP - 16);
+    for (uint64_t x = a;; x += span) {
+        uint64_t y = (b - x) >= span ? x + span - 2 : b;
+        DevRecord r;
+        int rc = run_piece_sync(d, x, y, &r, nullptr);
+        if (rc) return rc;
+        if (r.overflow) GB_FAIL(d, GB_ERR_INTERNAL, "straggler list overflow on a sub-piece");
+        rec_merge(into, r);
+        if (y == b) break;
+    }
+    return GB_OK;
+}
+
+static int batch_complete(gb_dev* d, int bi) {
+    Batch& b = d->batches[bi];
+    CU(d, cudaEventSynchronize(b.ev_done));
+    CU(d, cudaGetLastError());
+    if (b.timed) {
+        float ms = 0;
+        if (b.large && cudaEventElapsedTime(&ms, b.ev_l0, b.ev_k0) == cudaSuccess) {
+            d->kms[1] += ms;
+            d->kl[1] += 1;
+        }
+        if (cudaEventElapsedTime(&ms, b.ev_k0, b.ev_k1) == cudaSuccess) {
+            d->kms[0] += ms;
+            d->kl[0] += 1;
+        }
+        if (cudaEventElapsedTime(&ms, b.ev_k1, b.ev_s1) == cudaSuccess) {
+            d->kms[2] += ms;
+            d->kl[2] += 2;
+        }
+    }
+    double t = now_s();
+    for (size_t s = 0; s < b.pieces.size(); ++s) {
+        UserSeg* u = find_seg(d, b.pieces[s].seq);
+        if (!u) GB_FAIL(d, GB_ERR_INTERNAL, "completed piece has no owner");
+        const DevRecord& r = b.h_rec[s];
+        if (r.overflow) {
+            int rc = rerun_split(d, b.pieces[s].a, b.pieces[s].b, u->rec);
+            if (rc) return rc;
+        } else {
+            rec_merge(u->rec, r);
+        }
+        u->pieces_done++;
+        if (u->pieces_done == u->pieces_total) u->rec.elapsed_seconds = t - u->t0;
+    }
+    b.pieces.clear();
+    b.launched = false;
+    return GB_OK;
+}
+
+static int launch_fill(gb_dev* d) {
+    if (d->fill < 0) return GB_OK;
+    Batch& b = d->batches[d->fill];
+    if (b.pieces.empty()) return GB_OK;
+    int rc = batch_launch(d, b, nullptr);
+    if (rc) return rc;
+    d->inflight.push_back(d->fill);
+    d->fill = -1;
+    return GB_OK;
+}
+
+static int acquire_fill(gb_dev* d) {
+    if (d->fill >= 0) return GB_OK;
+    for (;;) {
+        for (int i = 0; i < NBATCH; ++i) {
+            Batch& b = d->batches[i];
+            bool busy = b.launched || !b.pieces.empty();
+            if (!busy) {
+                d->fill = i;
+                return GB_OK;
+            }
+        }
+        // all batches in flight: retire the oldest
+        if (d->inflight.empty()) GB_FAIL(d, GB_ERR_INTERNAL, "no free batch");
+        int bi = d->inflight.front();
+        d->inflight.pop_front();
+        int rc = batch_complete(d, bi);
+        if (rc) return rc;
+    }
+}
+
+static int check_segment(gb_dev* d, uint64_t a, uint64_t b) {
+    // check_job (verifier.cpp:15-20)
+    if ((a & 1) || (b & 1)) GB_FAIL(d, GB_ERR_PARAM, "segment bounds must be even");
+    if (a < 4 || a > b) GB_FAIL(d, GB_ERR_PARAM, "segment must satisfy 4 <= a <= b");
+    // sieve_range_for (verifier.cpp:35-43) and the coverage check of
+    // tiled_sieve_segment (sieve.cpp:100-103)
+    uint64_t lo = a > d->prm.p_small ? a - d->prm.p_small : 0;
+    if (lo < 3) lo = 3;
+    if ((lo & 1) == 0) ++lo;
+    uint64_t hi = b - 3;
+    if (hi < lo) hi = lo;
+    uint64_t s = d->sqrt_bound;
+    if (s == 0 || s < hi / s)
+        GB_FAIL(d, GB_ERR_PARAM, "tiled_sieve_segment: base primes insufficient for segment bound");
+    return GB_OK;
+}
+
+// --------------------------------------------------------------- K1 build
+static int build_tables(gb_dev* d) {
+    const uint64_t s = d->sqrt_bound;
+    CU(d, cudaMalloc(&d->d_pat, PAT_WORDS * 4));
+    CU(d, cudaMalloc(&d->d_pmr, NWIN * 8));
+    cudaStream_t st = d->sync.st;
+    CU(d, launch_init_tables(d->d_pat, d->d_pmr, d->prm.p_small, st));
+    d->launches++;
+    if (s < 3) {
+        d->n_primes = 0;
+        CU(d, cudaMalloc(&d->d_primes, 4));
+        CU(d, cudaStreamSynchronize(st));
+        return GB_OK;
+    }
+    // seeds: odd primes <= isqrt(s) (<= 65536)
+    uint32_t lim = (uint32_t)std::min<uint64_t>(isqrt_floor(s) + 1, 65536);
+    if (lim < 3) lim = 3;
+    uint32_t *d_seed = nullptr, *d_nseed = nullptr;
+    CU(d, cudaMalloc(&d_seed, 8192 * 4));
+    CU(d, cudaMalloc(&d_nseed, 4));
+    CU(d, launch_seed_primes(lim, d_seed, d_nseed, st));
+    uint32_t nseed = 0;
+    CU(d, cudaMemcpyAsync(&nseed, d_nseed, 4, cudaMemcpyDeviceToHost, st));
+    CU(d, cudaStreamSynchronize(st));
+    std::vector<uint32_t> hseed(nseed);
+    if (nseed) CU(d, cudaMemcpy(hseed.data(), d_seed, nseed * 4, cudaMemcpyDeviceToHost));
+    uint32_t sA0 = (uint32_t)(std::lower_bound(hseed.begin(), hseed.end(), FIRST_STRIKE_P) - hseed.begin());
+    uint32_t sA1 = (uint32_t)(std::lower_bound(hseed.begin(), hseed.end(), P_WARP_MAX) - hseed.begin());
+    // sieve [3, s] on device
+    const uint64_t n_cells = (s - 3) / 2 + 1;
+    const uint64_t n_words = (n_cells + 31) / 32;
+    uint32_t* d_bits = nullptr;
+    CU(d, cudaMalloc(&d_bits, (n_words + 1) * 4));
+    int grid = d->sms * 2;
+    CU(d, launch_sieve_interval(3, n_cells, d_seed, sA0, sA1, nseed, d->d_pat, d_bits, grid, st));
+    const uint32_t chunk = 4096;
+    const uint64_t n_chunks = (n_words + chunk - 1) / chunk;
+    uint32_t* d_counts = nullptr;
+    uint64_t *d_off = nullptr, *d_total = nullptr;
+    CU(d, cudaMalloc(&d_counts, n_chunks * 4));
+    CU(d, cudaMalloc(&d_off, n_chunks * 8));
+    CU(d, cudaMalloc(&d_total, 8));
+    CU(d, launch_count_words(d_bits, n_words, chunk, d_counts, n_chunks, st));
+    CU(d, launch_scan(d_counts, n_chunks, d_off, d_total, st));
+    uint64_t total = 0;
+    CU(d, cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, st));
+    CU(d, cudaStreamSynchronize(st));
+    CU(d, cudaMalloc(&d->d_primes, std::max<uint64_t>(total, 1) * 4));
+    CU(d, launch_compact(d_bits, n_words, chunk, d_off, 3, d->d_primes, n_chunks, st));
+    d->launches += 5;
+    CU(d, cudaStreamSynchronize(st));
+    cudaFree(d_bits);
+    cudaFree(d_counts);
+    cudaFree(d_off);
+    cudaFree(d_total);
+    cudaFree(d_seed);
+    cudaFree(d_nseed);
+    d->n_primes = total;
+    // index ranges (primes <= P_TILE_MAX are the first pi(2^22) entries)
+    uint64_t head = std::min<uint64_t>(total, 300000);
+    std::vector<uint32_t> hp(head);
+    if (head) CU(d, cudaMemcpy(hp.data(), d->d_primes, head * 4, cudaMemcpyDeviceToHost));
+    d->iA0 = (uint32_t)(std::lower_bound(hp.begin(), hp.end(), FIRST_STRIKE_P) - hp.begin());
+    d->iA1 = (uint32_t)(std::lower_bound(hp.begin(), hp.end(), P_WARP_MAX) - hp.begin());
+    d->iB1 = (uint32_t)(std::upper_bound(hp.begin(), hp.end(), P_TILE_MAX) - hp.begin());
+    d->iL0 = d->iB1;
+    d->iL1 = total;
+    return GB_OK;
+}
+
+// --------------------------------------------------------------- C-ABI
+extern "C" {
+
+const char* gb_version(void) { return "goldbach_b200 1.0 (sm_100a)"; }
+
+int gb_device_count(int* count) {
+    int n = 0;
+    cudaError_t e = cudaGetDeviceCount(&n);
+    if (e != cudaSuccess) n = 0;
+    *count = n;
+    return GB_OK;
+}
+
+int gb_open(int device, const gb_params* params, gb_dev** out) {
+    *out = nullptr;
+    if (!params) GB_FAIL(nullptr, GB_ERR_PARAM, "gb_open: params is NULL");
+    if (params->p_small < 3) GB_FAIL(nullptr, GB_ERR_PARAM, "SmallPrimeTable: p_small must be >= 3");
+    if (params->cover_limit < 1) GB_FAIL(nullptr, GB_ERR_PARAM, "build_base_primes: cover_limit must be >= 1");
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
+        GB_FAIL(nullptr, GB_ERR_CUDA, "gb_open: no CUDA device available");
+    if (device < 0 || device >= n) GB_FAIL(nullptr, GB_ERR_PARAM, "gb_open: device index out of range");
+    gb_dev* d = new gb_dev();
+    d->device = device;
+    d->prm = *params;
+    if (d->prm.max_seg_evens == 0) d->prm.max_seg_evens = 200000000ull;
+    int rc = GB_OK;
+    do {
+        if (cudaSetDevice(device) != cudaSuccess) {
+            set_err(d, "cudaSetDevice failed");
+            rc = GB_ERR_CUDA;
+            break;
+        }
+        cudaDeviceProp prop;
+        cudaGetDeviceProperties(&prop, device);
+        if (prop.major != 10) {
+            set_err(d, std::string("gb_open: built for sm_100a, device is ") + prop.name);
+            rc = GB_ERR_CUDA;
+            break;
+        }
+        d->sms = prop.multiProcessorCount;
+        int occ = 0;
+        if (verify_occupancy(&occ) != 0 || occ < 1) {
+            set_err(d, "gb_open: fused kernel cannot be resident (shared memory)");
+            rc = GB_ERR_RESOURCE;
+            break;
+        }
+        d->occ = occ;
+        d->sqrt_bound = sqrt_bound_of(params->cover_limit);
+        if (cudaStreamCreateWithFlags(&d->sync.st, cudaStreamNonBlocking) != cudaSuccess) {
+            set_err(d, "gb_open: cudaStreamCreate failed");
+            rc = GB_ERR_CUDA;
+            break;
+        }
+        if ((rc = build_tables(d)) != GB_OK) break;
+        d->max_piece = std::min<uint64_t>(d->prm.max_seg_evens, MAX_PIECE);
+        uint64_t blocks = (d->max_piece + E - 1) / E;
+        d->qg_stride = (blocks * E + JH + 31) / 32;
+        if ((rc = batch_alloc(d, d->sync, true)) != GB_OK) break;
+        for (int i = 0; i < NBATCH && rc == GB_OK; ++i) rc = batch_alloc(d, d->batches[i], true);
+    } while (false);
+    if (rc != GB_OK) {
+        t_err = d->err;
+        gb_close(d);
+        return rc;
+    }
+    *out = d;
+    return GB_OK;
+}
+
+int gb_close(gb_dev* d) {
+    if (!d) return GB_OK;
+    cudaSetDevice(d->device);
+    cudaDeviceSynchronize();
+    for (auto& b : d->batches) batch_free(b);
+    batch_free(d->sync);
+    cudaFree(d->d_primes);
+    cudaFree(d->d_pat);
+    cudaFree(d->d_pmr);
+    delete d;
+    return GB_OK;
+}
+
+const char* gb_last_error(const gb_dev* d) { return d ? d->err.c_str() : t_err.c_str(); }
+
+int gb_set_inject_fail(gb_dev* d, uint64_t inject_fail) {
+    if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
+    d->prm.inject_fail = inject_fail;
+    return GB_OK;
+}
+
+int gb_max_inflight(const gb_dev* d, int* depth) {
+    (void)d;
+    *depth = NBATCH * SLOTS;
+    return GB_OK;
+}
+
+int gb_submit_segment(gb_dev* d, uint64_t a, uint64_t b, uint64_t tag) {
+    if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
+    int rc = check_segment(d, a, b);
+    if (rc) return rc;
+    CU(d, cudaSetDevice(d->device));
+    UserSeg u;
+    u.seq = d->next_seq++;
+    u.a = a;
+    u.b = b;
+    u.tag = tag;
+    u.t0 = now_s();
+    u.rec.a = a;
+    u.rec.b = b;
+    const uint64_t span = 2 * d->max_piece;
+    std::vector<Piece> pcs;
+    for (uint64_t x = a;; x += span) {
+        uint64_t y = (b - x) >= span ? x + span - 2 : b;
+        pcs.push_back(Piece{u.seq, x, y});
+        if (y == b) break;
+    }
+    u.pieces_total = (uint32_t)pcs.size();
+    d->segs.push_back(u);
+    for (const Piece& pc : pcs) {
+        if ((rc = acquire_fill(d)) != GB_OK) return rc;
+        Batch& fb = d->batches[d->fill];
+        fb.pieces.push_back(pc);
+        if (fb.pieces.size() == SLOTS)
+            if ((rc = launch_fill(d)) != GB_OK) return rc;
+    }
+    // keep the device busy: launch a partial batch if nothing is running
+    if (d->inflight.empty()) rc = launch_fill(d);
+    return rc;
+}
+
+int gb_wait_segment(gb_dev* d, gb_seg_record* out, uint64_t* tag) {
+    if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
+    if (d->segs.empty()) GB_FAIL(d, GB_ERR_PARAM, "gb_wait_segment: nothing submitted");
+    CU(d, cudaSetDevice(d->device));
+    int rc;
+    while (d->segs.front().pieces_done < d->segs.front().pieces_total) {
+        if (d->inflight.empty()) {
+            if (d->fill < 0) GB_FAIL(d, GB_ERR_INTERNAL, "pending segment with no batch");
+            if ((rc = launch_fill(d)) != GB_OK) return rc;
+            continue;
+        }
+        // launch the partial batch first so it overlaps the wait
+        if (d->fill >= 0 && !d->batches[d->fill].pieces.empty() && (int)d->inflight.size() < NBATCH)
+            if ((rc = launch_fill(d)) != GB_OK) return rc;
+        int bi = d->inflight.front();
+        d->inflight.pop_front();
+        if ((rc = batch_complete(d, bi)) != GB_OK) return rc;
+    }
+    UserSeg u = d->segs.front();
+    d->segs.pop_front();
+    *out = u.rec;
+    if (tag) *tag = u.tag;
+    return GB_OK;
+}
+
+int gb_verify_segment(gb_dev* d, uint64_t a, uint64_t b, gb_seg_record* out) {
+    if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
+    if (!d->segs.empty()) GB_FAIL(d, GB_ERR_PARAM, "gb_verify_segment: asynchronous segments pending");
+    int rc = gb_submit_segment(d, a, b, 0);
+    if (rc) return rc;
+    return gb_wait_segment(d, out, nullptr);
+}
+
+int gb_base_primes(gb_dev* d, uint64_t* sqrt_bound, uint64_t* count, uint32_t* out, uint64_t cap) {
+    if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
+    CU(d, cudaSetDevice(d->device));
+    if (sqrt_bound) *sqrt_bound = d->sqrt_bound;
+    if (count) *count = d->n_primes;
+    if (out && cap) {
+        uint64_t n = std::min(cap, d->n_primes);
+        if (n) CU(d, cudaMemcpy(out, d->d_primes, n * 4, cudaMemcpyDeviceToHost));
+    }
+    return GB_OK;
+}
+
+int gb_sieve_interval(gb_dev* d, uint64_t lo, uint64_t hi, uint64_t* words, uint64_t n_words) {
+    if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
+    if ((lo & 1) == 0 || (hi & 1) == 0) GB_FAIL(d, GB_ERR_PARAM, "tiled_sieve_segment: bounds must be odd");
+    if (lo > hi) GB_FAIL(d, GB_ERR_PARAM, "tiled_sieve_segment: lo must be <= hi");
+    uint64_t s = d->sqrt_bound;
+    if (s == 0 || s < hi / s)
+        GB_FAIL(d, GB_ERR_PARAM, "tiled_sieve_segment: base primes insufficient for segment bound");
+    const uint64_t n_cells = ((hi - lo) >> 1) + 1;
+    const uint64_t need = (n_cells + 63) / 64;
+    if (n_words < need) GB_FAIL(d, GB_ERR_PARAM, "gb_sieve_interval: output too small");
+    CU(d, cudaSetDevice(d->device));
+    cudaStream_t st = d->sync.st;
+    uint32_t* d_bits = nullptr;
+    CU(d, cudaMalloc(&d_bits, need * 8 + 8));
+    CU(d, cudaMemsetAsync(d_bits, 0, need * 8 + 8, st));
+    int grid = (int)std::min<uint64_t>((n_cells + W - 1) / W, (uint64_t)d->sms * 2);
+    // every base prime (p^2 beyond hi strikes nothing)
+    CU(d, launch_sieve_interval(lo, n_cells, d->d_primes, d->iA0, d->iA1, (uint32_t)d->n_primes, d->d_pat, d_bits,
+                                grid, st));
+    d->launches++;
+    CU(d, cudaMemcpyAsync(words, d_bits, need * 8, cudaMemcpyDeviceToHost, st));
+    CU(d, cudaStreamSynchronize(st));
+    cudaFree(d_bits);
+    return GB_OK;
+}
+
+int gb_phase1_pmin(gb_dev* d, uint64_t a, uint64_t b, uint64_t* out, uint64_t n_out) {
+    if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
+    int rc = check_segment(d, a, b);
+    if (rc) return rc;
+    uint64_t n = ((b - a) >> 1) + 1;
+    if (n_out < n) GB_FAIL(d, GB_ERR_PARAM, "gb_phase1_pmin: output too small");
+    if (n > LIST_CAP - 16) GB_FAIL(d, GB_ERR_PARAM, "gb_phase1_pmin: at most 2^20 evens per call");
+    CU(d, cudaSetDevice(d->device));
+    uint64_t* d_out = nullptr;
+    CU(d, cudaMalloc(&d_out, n * 8));
+    DevRecord r;
+    rc = run_piece_sync(d, a, b, &r, d_out);
+    if (rc == GB_OK) CU(d, cudaMemcpy(out, d_out, n * 8, cudaMemcpyDeviceToHost));
+    cudaFree(d_out);
+    return rc;
+}
+
+int gb_is_prime_batch(gb_dev* d, const uint64_t* values, uint8_t* out, uint64_t count) {
+    if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
+    if (!count) return GB_OK;
+    CU(d, cudaSetDevice(d->device));
+    cudaStream_t st = d->sync.st;
+    uint64_t* dv = nullptr;
+    uint8_t* dout = nullptr;
+    CU(d, cudaMalloc(&dv, count * 8));
+    CU(d, cudaMalloc(&dout, count));
+    CU(d, cudaMemcpyAsync(dv, values, count * 8, cudaMemcpyHostToDevice, st));
+    CU(d, launch_is_prime_batch(dv, dout, count, st));
+    d->launches++;
+    CU(d, cudaMemcpyAsync(out, dout, count, cudaMemcpyDeviceToHost, st));
+    CU(d, cudaStreamSynchronize(st));
+    cudaFree(dv);
+    cudaFree(dout);
+    return GB_OK;
+}
+
+int gb_phase2_resolve(gb_dev* d, uint64_t n, uint64_t* p) {
+    if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
+    if (n < 4 || (n & 1)) GB_FAIL(d, GB_ERR_PARAM, "phase2_resolve: n must be even and >= 4");
+    CU(d, cudaSetDevice(d->device));
+    cudaStream_t st = d->sync.st;
+    uint64_t* dp = nullptr;
+    CU(d, cudaMalloc(&dp, 8));
+    CU(d, launch_phase2_one(n, dp, st));
+    d->launches++;
+    CU(d, cudaMemcpyAsync(p, dp, 8, cudaMemcpyDeviceToHost, st));
+    CU(d, cudaStreamSynchronize(st));
+    cudaFree(dp);
+    return GB_OK;
+}
+
+int gb_launch_count(const gb_dev* d, uint64_t* launches) {
+    if (!d) return GB_ERR_PARAM;
+    *launches = d->launches;
+    return GB_OK;
+}
+
+int gb_kernel_times(gb_dev* d, double* ms4, uint64_t* launches4, int reset) {
+    if (!d) return GB_ERR_PARAM;
+    for (int i = 0; i < 4; ++i) {
+        if (ms4) ms4[i] = d->kms[i];
+        if (launches4) launches4[i] = d->kl[i];
+        if (reset) {
+            d->kms[i] = 0;
+            d->kl[i] = 0;
+        }
+    }
+    return GB_OK;
+}
+
+int gb_set_timing(gb_dev* d, int enabled) {
+    if (!d) return GB_ERR_PARAM;
+    d->timing = enabled != 0;
+    return GB_OK;
+}
+
+} // extern "C"

@@ -176,7 +176,7 @@ __global__ void __launch_bounds__(THREADS) k_sieve_interval(uint64_t lo, uint64_
                                                             uint32_t iA0, uint32_t iA1, uint32_t iB1,
                                                             const uint32_t* __restrict__ gpat,
                                                             uint32_t* __restrict__ out) {
-    extern __shared__ uint32_t smem[];
+    extern __shared__ __align__(16) uint32_t smem[];
     uint32_t* tile = smem;                       // TILE_WORDS + 1
     uint32_t* pat = smem + TILE_WORDS + 1;       // PAT_WORDS
     for (uint32_t i = threadIdx.x; i < PAT_WORDS; i += blockDim.x) pat[i] = gpat[i];
@@ -366,16 +366,16 @@ __device__ __forceinline__ uint64_t window_bits(const uint32_t* tile, int64_t x)
 }
 
 __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
-    extern __shared__ uint32_t smem[];
-    uint32_t* tile = smem;                                  // TILE_WORDS + 3 (pad)
-    uint32_t* pat = smem + TILE_WORDS + 3;                  // PAT_WORDS
-    uint64_t* pmr = (uint64_t*)(pat + PAT_WORDS + (PAT_WORDS & 1)); // NWIN
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t* tile = smem;                                  // TILE_WORDS + pad
+    uint32_t* pat = smem + VERIFY_PAT_OFF;                  // PAT_WORDS
+    uint64_t* pmr = (uint64_t*)(smem + VERIFY_PMR_OFF);     // NWIN
     __shared__ uint32_t s_blk;
     __shared__ unsigned long long s_red[NWARPS][3];
 
     for (uint32_t i = threadIdx.x; i < PAT_WORDS; i += blockDim.x) pat[i] = A.gpat[i];
     for (uint32_t i = threadIdx.x; i < (uint32_t)NWIN; i += blockDim.x) pmr[i] = A.pmr[i];
-    for (uint32_t i = threadIdx.x; i < 3; i += blockDim.x) tile[TILE_WORDS + i] = 0;
+    for (uint32_t i = threadIdx.x; i < 4; i += blockDim.x) tile[TILE_WORDS + i] = 0;
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t jlim_small = A.p_small >= 3 ? (uint32_t)min((A.p_small - 3) / 2, (uint64_t)0xFFFFFFFFu) : 0;
 
@@ -641,13 +641,6 @@ cudaError_t launch_seed_primes(uint32_t lim, uint32_t* out, uint32_t* count, cud
 cudaError_t launch_sieve_interval(uint64_t lo, uint64_t n_cells, const uint32_t* primes, uint32_t iA0,
                                   uint32_t iA1, uint32_t iB1, const uint32_t* pat, uint32_t* out,
                                   int grid, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_sieve_interval, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)SIEVE_SMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
     k_sieve_interval<<<grid, THREADS, SIEVE_SMEM, st>>>(lo, n_cells, primes, iA0, iA1, iB1, pat, out);
     return cudaGetLastError();
 }
@@ -683,13 +676,6 @@ cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint3
     return cudaGetLastError();
 }
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st) {
-    static bool attr = false;
-    if (!attr) {
-        cudaError_t e = cudaFuncSetAttribute(k_verify_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                             (int)VERIFY_SMEM);
-        if (e != cudaSuccess) return e;
-        attr = true;
-    }
     k_verify_blocks<<<grid, THREADS, VERIFY_SMEM, st>>>(a);
     return cudaGetLastError();
 }
@@ -716,7 +702,13 @@ cudaError_t launch_is_prime_batch(const uint64_t* v, uint8_t* out, uint64_t n, c
     return cudaGetLastError();
 }
 int verify_occupancy(int* blocks_per_sm) {
-    cudaFuncSetAttribute(k_verify_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)VERIFY_SMEM);
+    // per-device function attributes: call after cudaSetDevice
+    if (cudaFuncSetAttribute(k_verify_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)VERIFY_SMEM) !=
+        cudaSuccess)
+        return 1;
+    if (cudaFuncSetAttribute(k_sieve_interval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SIEVE_SMEM) !=
+        cudaSuccess)
+        return 1;
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_verify_blocks, THREADS,
                                                               VERIFY_SMEM);
 }

@@ -44,7 +44,10 @@ struct VerifyArgs {
 };
 
 // dynamic shared memory of the tile kernels
-constexpr size_t VERIFY_SMEM = (TILE_WORDS + 3 + PAT_WORDS + (PAT_WORDS & 1)) * 4 + NWIN * 8;
+// k_verify_blocks dynamic smem: [tile | 4 pad words][patterns][pmr (8-B aligned)]
+constexpr uint32_t VERIFY_PAT_OFF = TILE_WORDS + 4;
+constexpr uint32_t VERIFY_PMR_OFF = (VERIFY_PAT_OFF + PAT_WORDS + 3) & ~3u; // 16-B aligned, in words
+constexpr size_t VERIFY_SMEM = (size_t)VERIFY_PMR_OFF * 4 + NWIN * 8;
 constexpr size_t SIEVE_SMEM = (TILE_WORDS + 1 + PAT_WORDS) * 4;
 
 // ---- launchers (gb_kernels.cu); all asynchronous on `st`

@@ -1,0 +1,98 @@
+"""Device parity against golden vectors produced by the UNMODIFIED reference
+(oracle/make_goldens.py) and SURVEY.md Appendix A.  Bit-exact everywhere."""
+import hashlib
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+TOP = (1 << 64) - 1
+
+
+def rec_matches(rec, want):
+    got = rec.as_dict()
+    for k in ("a", "b", "evens", "unverified", "phase2", "sum_pmin", "pos_hash", "max_p",
+              "max_n", "n_ce", "ce"):
+        assert got[k] == want[k], (k, got, want)
+
+
+def test_base_primes_match_reference(gpu):
+    for t in golden("base_primes.json")["tables"]:
+        if t["cover"] < 1:
+            continue
+        with gpu.Device(t["cover"], p_small=1000) as dev:
+            s, n, primes = dev.base_primes()
+            assert s == t["sqrt_bound"], t["cover"]
+            assert n == t["count"], t["cover"]
+            if n:
+                assert [int(x) for x in primes[:8]] == t["first"]
+                assert [int(x) for x in primes[-8:]] == t["last"]
+                assert hashlib.sha256(primes.astype("<u4").tobytes()).hexdigest() == t["sha256"]
+
+
+def test_sieve_windows_match_reference(gpu):
+    for w in golden("sieve_windows.json")["windows"]:
+        with gpu.Device(w["cover"], p_small=1000) as dev:
+            words = dev.sieve_words(w["lo"], w["hi"])
+            assert int(sum(bin(int(x)).count("1") for x in words)) == w["popcount"], w
+            assert hashlib.sha256(words.astype("<u8").tobytes()).hexdigest() == w["sha256"], w
+
+
+def test_phase1_pmin_vectors_match_reference(gpu):
+    for v in golden("pmin_vectors.json")["vectors"]:
+        with gpu.Device(v["cover"], p_small=v["p_small"]) as dev:
+            got = dev.phase1_pmin(v["a"], v["b"])
+            want = np.array(v["pmin"], dtype=np.uint64)
+            bad = np.nonzero(got != want)[0]
+            assert len(bad) == 0, (v["a"], v["p_small"], bad[:5], got[bad[:5]], want[bad[:5]])
+
+
+def test_small_segments_match_reference(gpu):
+    for r in golden("segments_small.json")["records"]:
+        with gpu.Device(r["cover"], p_small=r["p_small"], inject_fail=r["inject"]) as dev:
+            rec_matches(dev.verify_segment(r["a"], r["b"]), r)
+
+
+def test_c1_appendix_a(gpu):
+    with gpu.Device(100_000_000) as dev:
+        r = dev.verify_segment(4, 100_000_000).as_dict()
+    assert r["evens"] == 49_999_999 and r["unverified"] == 0 and r["phase2"] == 0
+    assert r["sum_pmin"] == 1_511_603_116
+    assert r["pos_hash"] == 39_265_891_176_952_445
+    assert (r["max_p"], r["max_n"]) == (1093, 60_119_912)
+
+
+def test_c2_all_segments(gpu):
+    recs = golden("c2_segments.json")["records"]
+    with gpu.Device(10**10) as dev:
+        for r in recs:
+            dev.submit(r["a"], r["b"], tag=r["a"])
+        for r in recs:
+            got, tag = dev.wait()
+            assert tag == r["a"]
+            rec_matches(got, r)
+
+
+def test_ceiling_window(gpu):
+    r = golden("ceiling.json")["records"][0]
+    with gpu.Device(r["cover"], p_small=r["p_small"], max_seg_evens=50_000) as dev:
+        rec_matches(dev.verify_segment(r["a"], r["b"]), r)
+
+
+def test_device_primality_matches_reference(gpu):
+    vals = golden("primality.json")["values"]
+    with gpu.Device(1000) as dev:
+        got = dev.is_prime([v["n"] for v in vals])
+    for v, g in zip(vals, got):
+        assert bool(g) == v["prime"], v["n"]
+
+
+def test_device_phase2_matches_reference(gpu):
+    for c in golden("phase2.json")["cases"]:
+        if c["p_small"] != 3 and c["n"] > 10**6:
+            pass
+        with gpu.Device(1000, p_small=3) as dev:
+            assert dev.phase2_resolve(c["n"]) == c["p"], c
