@@ -138,6 +138,12 @@ int gb_wait_segment(gb_dev* dev, gb_seg_record* out, uint64_t* tag);
 int gb_base_primes(gb_dev* dev, uint64_t* sqrt_bound, uint64_t* count,
                    uint32_t* out, uint64_t cap);
 
+/* Odd primes <= limit (limit < 2^32) sieved on the device; copies up to
+ * cap into out when out != NULL.  Backs simple_sieve / SmallPrimeTable /
+ * Phase2Table::build of the C++ API (sieve.cpp:22-42). */
+int gb_primes_upto(gb_dev* dev, uint64_t limit, uint32_t* out, uint64_t cap,
+                   uint64_t* count);
+
 /* Device sieve of the odd interval [lo, hi] (lo, hi odd, lo <= hi):
  * writes ((hi-lo)/2 + 64) / 64 words, bit i <-> lo + 2i, LSB-first, slack
  * bits zero: the OddBitset layout of tiled_sieve_segment (sieve.cpp:91-156,
@@ -169,8 +175,21 @@ int gb_launch_count(const gb_dev* dev, uint64_t* launches);
  * (K2/K3 fused), [1]=large-prime strike, [2]=stragglers/Phase 2, [3]=other. */
 int gb_kernel_times(gb_dev* dev, double* ms4, uint64_t* launches4, int reset);
 
-/* Enable/disable per-launch event timing (adds two events per launch). */
+/* Per-launch event timing: 0 off, 1 on, 2 on with every batch serialised on
+ * one stream (so an event pair brackets exactly one kernel's execution;
+ * used for the roofline pass of bench.py).  No segments may be pending. */
 int gb_set_timing(gb_dev* dev, int enabled);
+
+/* Host<->device bytes moved by segment traffic since open (job descriptors
+ * in, records out). */
+int gb_io_bytes(const gb_dev* dev, uint64_t* h2d, uint64_t* d2h);
+
+/* Writes 256 MiB of scratch (> the 126 MB L2) and synchronises: evicts L2
+ * between timed iterations. */
+int gb_flush_l2(gb_dev* dev);
+
+/* cudaDeviceSynchronize on the handle's device. */
+int gb_synchronize(gb_dev* dev);
 
 #ifdef __cplusplus
 }

@@ -139,6 +139,10 @@ def lib():
         "gb_launch_count": ([vp, p64], i32),
         "gb_kernel_times": ([vp, C.POINTER(C.c_double), p64, i32], i32),
         "gb_set_timing": ([vp, i32], i32),
+        "gb_io_bytes": ([vp, p64, p64], i32),
+        "gb_flush_l2": ([vp], i32),
+        "gb_synchronize": ([vp], i32),
+        "gb_primes_upto": ([vp, u64, C.POINTER(C.c_uint32), u64, p64], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -158,8 +162,12 @@ def _bind_pool(L):
         "gb_pool_claim": ([vp, p64, p64, p64], i32),
         "gb_pool_destroy": ([vp, i32], i32),
         "gb_drain_pool": ([vp, vp, i32, C.POINTER(RunResult)], i32),
-        "gb_run_range": ([u64, u64, u64, u64, u64, C.POINTER(i32), i32, i32,
+        "gb_run_range": ([u64, u64, u64, u64, u64, C.POINTER(i32), i32, i32, i32,
                           C.POINTER(RunResult), p64], i32),
+        "gb_estimate_device_bytes": ([u64, u64, u64], u64),
+        "gb_device_memory": ([i32, p64, p64], i32),
+        "gb_pool_last_error": ([], C.c_char_p),
+        "gb_primes_upto": ([vp, u64, C.POINTER(C.c_uint32), u64, p64], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name, None)
@@ -294,8 +302,29 @@ class Device:
         _check(lib().gb_launch_count(self._h, C.byref(n)), self._h)
         return n.value
 
-    def set_timing(self, on: bool):
-        _check(lib().gb_set_timing(self._h, 1 if on else 0), self._h)
+    def set_timing(self, mode):
+        """0/False off, 1/True event timing, 2 timing with serialised batches."""
+        _check(lib().gb_set_timing(self._h, int(mode)), self._h)
+
+    def io_bytes(self):
+        h, d = C.c_uint64(), C.c_uint64()
+        _check(lib().gb_io_bytes(self._h, C.byref(h), C.byref(d)), self._h)
+        return h.value, d.value
+
+    def flush_l2(self):
+        _check(lib().gb_flush_l2(self._h), self._h)
+
+    def synchronize(self):
+        _check(lib().gb_synchronize(self._h), self._h)
+
+    def primes_upto(self, limit: int):
+        import numpy as np
+        n = C.c_uint64()
+        _check(lib().gb_primes_upto(self._h, limit, None, 0, C.byref(n)), self._h)
+        out = np.zeros(max(n.value, 1), dtype=np.uint32)
+        _check(lib().gb_primes_upto(self._h, limit, out.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                    n.value, C.byref(n)), self._h)
+        return out[: n.value]
 
     def kernel_times(self, reset: bool = False):
         ms = (C.c_double * 4)()
@@ -312,7 +341,9 @@ class Pool:
                  create: bool = True):
         h = C.c_void_p()
         name = shm_name.encode() if shm_name else None
-        _check(lib().gb_pool_create(start, limit, seg_size, name, 1 if create else 0, C.byref(h)))
+        rc = lib().gb_pool_create(start, limit, seg_size, name, 1 if create else 0, C.byref(h))
+        if rc:
+            raise _ERRS.get(rc, GoldbachError)(lib().gb_pool_last_error().decode(errors="replace"))
         self._h = h
         self.shm_name = shm_name
         self.owner = create
@@ -321,7 +352,7 @@ class Pool:
         a, b, i = C.c_uint64(), C.c_uint64(), C.c_uint64()
         rc = lib().gb_pool_claim(self._h, C.byref(a), C.byref(b), C.byref(i))
         if rc < 0:
-            _check(-rc)
+            raise _ERRS.get(-rc, GoldbachError)("gb_pool_claim failed")
         return (a.value, b.value, i.value) if rc == 1 else None
 
     def close(self, unlink: Optional[bool] = None):
@@ -338,6 +369,11 @@ class Pool:
     @property
     def handle(self):
         return self._h
+
+
+def estimate_device_bytes(cover_limit: int, p_small: int = 1_000_000,
+                          max_seg_evens: int = 200_000_000) -> int:
+    return lib().gb_estimate_device_bytes(cover_limit, p_small, max_seg_evens)
 
 
 def drain_pool(dev: Device, pool: Pool, max_inflight: int = 0) -> RunResult:
@@ -357,6 +393,8 @@ def run_range(start: int, limit: int, seg_size: int = 200_000_000, p_small: int 
     arr = (C.c_int * len(devs))(*devs)
     res = RunResult()
     per = (C.c_uint64 * max(k, 1))()
-    _check(lib().gb_run_range(start, limit, seg_size, p_small, inject_fail, arr, len(devs) if k is None else k,
-                              1 if progress else 0, C.byref(res), per))
+    rc = lib().gb_run_range(start, limit, seg_size, p_small, inject_fail, arr, len(devs), k,
+                            1 if progress else 0, C.byref(res), per)
+    if rc:
+        raise _ERRS.get(rc, GoldbachError)(lib().gb_pool_last_error().decode(errors="replace"))
     return res, list(per)[:k]

@@ -105,6 +105,9 @@ struct gb_dev {
     uint64_t next_seq = 0;
     uint64_t launches = 0;
     bool timing = false;
+    bool serial = false;           // timing mode 2: every batch on one stream
+    uint64_t h2d_bytes = 0, d2h_bytes = 0;
+    void* flush_buf = nullptr;
     double kms[4] = {0, 0, 0, 0};
     uint64_t kl[4] = {0, 0, 0, 0};
     Batch sync;                    // private batch for the synchronous helpers
@@ -198,7 +201,9 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
         large |= b.h_jobs[s].qg_words != 0;
     }
     b.large = large;
-    cudaStream_t st = b.st;
+    cudaStream_t st = d->serial ? d->sync.st : b.st;
+    d->h2d_bytes += n * sizeof(SegJob);
+    d->d2h_bytes += n * sizeof(DevRecord);
     CU(d, cudaMemcpyAsync(b.d_jobs, b.h_jobs, n * sizeof(SegJob), cudaMemcpyHostToDevice, st));
     CU(d, cudaMemsetAsync(b.d_acc, 0, n * sizeof(SlotAcc), st));
     CU(d, cudaMemsetAsync(b.d_counters, 0, 4 * sizeof(unsigned int), st));
@@ -399,21 +404,19 @@ static int check_segment(gb_dev* d, uint64_t a, uint64_t b) {
 }
 
 // --------------------------------------------------------------- K1 build
-static int build_tables(gb_dev* d) {
-    const uint64_t s = d->sqrt_bound;
-    CU(d, cudaMalloc(&d->d_pat, PAT_WORDS * 4));
-    CU(d, cudaMalloc(&d->d_pmr, NWIN * 8));
+// Odd primes <= L (L >= 3, L < 2^32 + 2^17) into a new device array: seed
+// primes by one CTA, segmented sieve of [3, L] with the tile machinery,
+// count / scan / compact.  build_base_primes semantics (sieve.cpp:44-70)
+// when L = sqrt_bound.
+static int device_odd_primes_upto(gb_dev* d, uint64_t L, uint32_t** d_out, uint64_t* count) {
     cudaStream_t st = d->sync.st;
-    CU(d, launch_init_tables(d->d_pat, d->d_pmr, d->prm.p_small, st));
-    d->launches++;
-    if (s < 3) {
-        d->n_primes = 0;
-        CU(d, cudaMalloc(&d->d_primes, 4));
-        CU(d, cudaStreamSynchronize(st));
+    *d_out = nullptr;
+    *count = 0;
+    if (L < 3) {
+        CU(d, cudaMalloc(d_out, 4));
         return GB_OK;
     }
-    // seeds: odd primes <= isqrt(s) (<= 65536)
-    uint32_t lim = (uint32_t)std::min<uint64_t>(isqrt_floor(s) + 1, 65536);
+    uint32_t lim = (uint32_t)std::min<uint64_t>(isqrt_floor(L) + 1, 65536);
     if (lim < 3) lim = 3;
     uint32_t *d_seed = nullptr, *d_nseed = nullptr;
     CU(d, cudaMalloc(&d_seed, 8192 * 4));
@@ -426,12 +429,11 @@ static int build_tables(gb_dev* d) {
     if (nseed) CU(d, cudaMemcpy(hseed.data(), d_seed, nseed * 4, cudaMemcpyDeviceToHost));
     uint32_t sA0 = (uint32_t)(std::lower_bound(hseed.begin(), hseed.end(), FIRST_STRIKE_P) - hseed.begin());
     uint32_t sA1 = (uint32_t)(std::lower_bound(hseed.begin(), hseed.end(), P_WARP_MAX) - hseed.begin());
-    // sieve [3, s] on device
-    const uint64_t n_cells = (s - 3) / 2 + 1;
+    const uint64_t n_cells = (L - 3) / 2 + 1;
     const uint64_t n_words = (n_cells + 31) / 32;
     uint32_t* d_bits = nullptr;
     CU(d, cudaMalloc(&d_bits, (n_words + 1) * 4));
-    int grid = d->sms * 2;
+    int grid = (int)std::min<uint64_t>((n_cells + W - 1) / W, (uint64_t)d->sms * 2);
     CU(d, launch_sieve_interval(3, n_cells, d_seed, sA0, sA1, nseed, d->d_pat, d_bits, grid, st));
     const uint32_t chunk = 4096;
     const uint64_t n_chunks = (n_words + chunk - 1) / chunk;
@@ -445,9 +447,9 @@ static int build_tables(gb_dev* d) {
     uint64_t total = 0;
     CU(d, cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, st));
     CU(d, cudaStreamSynchronize(st));
-    CU(d, cudaMalloc(&d->d_primes, std::max<uint64_t>(total, 1) * 4));
-    CU(d, launch_compact(d_bits, n_words, chunk, d_off, 3, d->d_primes, n_chunks, st));
-    d->launches += 5;
+    CU(d, cudaMalloc(d_out, std::max<uint64_t>(total, 1) * 4));
+    CU(d, launch_compact(d_bits, n_words, chunk, d_off, 3, *d_out, n_chunks, st));
+    d->launches += 6;
     CU(d, cudaStreamSynchronize(st));
     cudaFree(d_bits);
     cudaFree(d_counts);
@@ -455,7 +457,18 @@ static int build_tables(gb_dev* d) {
     cudaFree(d_total);
     cudaFree(d_seed);
     cudaFree(d_nseed);
-    d->n_primes = total;
+    *count = total;
+    return GB_OK;
+}
+
+static int build_tables(gb_dev* d) {
+    CU(d, cudaMalloc(&d->d_pat, PAT_WORDS * 4));
+    CU(d, cudaMalloc(&d->d_pmr, NWIN * 8));
+    CU(d, launch_init_tables(d->d_pat, d->d_pmr, d->prm.p_small, d->sync.st));
+    d->launches++;
+    int rc = device_odd_primes_upto(d, d->sqrt_bound, &d->d_primes, &d->n_primes);
+    if (rc) return rc;
+    const uint64_t total = d->n_primes;
     // index ranges (primes <= P_TILE_MAX are the first pi(2^22) entries)
     uint64_t head = std::min<uint64_t>(total, 300000);
     std::vector<uint32_t> hp(head);
@@ -466,6 +479,11 @@ static int build_tables(gb_dev* d) {
     d->iL0 = d->iB1;
     d->iL1 = total;
     return GB_OK;
+}
+
+static uint64_t pi_upper(uint64_t x) { // Rosser-Schoenfeld style bound, sizing only
+    if (x < 17) return 8;
+    return (uint64_t)(1.26 * (double)x / std::log((double)x)) + 1;
 }
 
 // --------------------------------------------------------------- C-ABI
@@ -545,6 +563,7 @@ int gb_close(gb_dev* d) {
     for (auto& b : d->batches) batch_free(b);
     batch_free(d->sync);
     cudaFree(d->d_primes);
+    cudaFree(d->flush_buf);
     cudaFree(d->d_pat);
     cudaFree(d->d_pmr);
     delete d;
@@ -721,6 +740,53 @@ int gb_phase2_resolve(gb_dev* d, uint64_t n, uint64_t* p) {
     return GB_OK;
 }
 
+int gb_primes_upto(gb_dev* d, uint64_t limit, uint32_t* out, uint64_t cap, uint64_t* count) {
+    if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
+    if (limit > 0xFFFFFFFFull) GB_FAIL(d, GB_ERR_RESOURCE, "gb_primes_upto: limit must be < 2^32");
+    CU(d, cudaSetDevice(d->device));
+    uint32_t* dp = nullptr;
+    uint64_t n = 0;
+    int rc = device_odd_primes_upto(d, limit, &dp, &n);
+    if (rc) return rc;
+    if (count) *count = n;
+    if (out && cap) {
+        uint64_t m = std::min(cap, n);
+        if (m) CU(d, cudaMemcpy(out, dp, m * 4, cudaMemcpyDeviceToHost));
+    }
+    cudaFree(dp);
+    return GB_OK;
+}
+
+uint64_t gb_estimate_device_bytes(uint64_t cover_limit, uint64_t p_small, uint64_t max_seg_evens) {
+    (void)p_small;
+    if (max_seg_evens == 0) max_seg_evens = 200000000ull;
+    const uint64_t s = sqrt_bound_of(cover_limit ? cover_limit : 1);
+    const uint64_t np_all = pi_upper(s);
+    const uint64_t np_tile = std::min<uint64_t>(np_all, pi_upper(P_TILE_MAX));
+    const uint64_t piece = std::min<uint64_t>(max_seg_evens, MAX_PIECE);
+    const uint64_t qg = s > P_TILE_MAX ? SLOTS * (((piece + E - 1) / E) * E + JH + 31) / 32 * 4 : 0;
+    const uint64_t per_batch = SLOTS * np_tile * 4 + qg + (uint64_t)LIST_CAP * (sizeof(StragEntry) + sizeof(StragResult)) +
+                               SLOTS * (sizeof(SegJob) + sizeof(SlotAcc) + sizeof(DevRecord)) + 64;
+    // base primes + K1 scratch bitmap (transient) + NBATCH + 1 batches
+    return np_all * 4 + (s / 16 + 64) + (uint64_t)(NBATCH + 1) * per_batch;
+}
+
+int gb_device_memory(int device, uint64_t* free_bytes, uint64_t* total_bytes) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n)
+        GB_FAIL(nullptr, GB_ERR_PARAM, "gb_device_memory: no such device");
+    int prev = 0;
+    cudaGetDevice(&prev);
+    cudaSetDevice(device);
+    size_t fr = 0, tot = 0;
+    cudaError_t e = cudaMemGetInfo(&fr, &tot);
+    cudaSetDevice(prev);
+    if (e != cudaSuccess) GB_FAIL(nullptr, GB_ERR_CUDA, cudaGetErrorString(e));
+    *free_bytes = fr;
+    *total_bytes = tot;
+    return GB_OK;
+}
+
 int gb_launch_count(const gb_dev* d, uint64_t* launches) {
     if (!d) return GB_ERR_PARAM;
     *launches = d->launches;
@@ -742,7 +808,33 @@ int gb_kernel_times(gb_dev* d, double* ms4, uint64_t* launches4, int reset) {
 
 int gb_set_timing(gb_dev* d, int enabled) {
     if (!d) return GB_ERR_PARAM;
+    if (!d->segs.empty()) GB_FAIL(d, GB_ERR_PARAM, "gb_set_timing: segments pending");
     d->timing = enabled != 0;
+    d->serial = enabled == 2;
+    return GB_OK;
+}
+
+int gb_io_bytes(const gb_dev* d, uint64_t* h2d, uint64_t* d2h) {
+    if (!d) return GB_ERR_PARAM;
+    if (h2d) *h2d = d->h2d_bytes;
+    if (d2h) *d2h = d->d2h_bytes;
+    return GB_OK;
+}
+
+int gb_flush_l2(gb_dev* d) {
+    if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
+    CU(d, cudaSetDevice(d->device));
+    const size_t bytes = 256ull << 20; // > 126 MB L2
+    if (!d->flush_buf) CU(d, cudaMalloc(&d->flush_buf, bytes));
+    CU(d, cudaMemsetAsync(d->flush_buf, d->launches & 0xff, bytes, d->sync.st));
+    CU(d, cudaStreamSynchronize(d->sync.st));
+    return GB_OK;
+}
+
+int gb_synchronize(gb_dev* d) {
+    if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
+    CU(d, cudaSetDevice(d->device));
+    CU(d, cudaDeviceSynchronize());
     return GB_OK;
 }
 

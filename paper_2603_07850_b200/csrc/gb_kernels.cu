@@ -132,16 +132,18 @@ __device__ __forceinline__ void strike(uint32_t* tile, uint32_t c) {
     atomicAnd(&tile[c >> 5], ~(1u << (c & 31)));
 }
 
-// warp-cooperative strikes (p < P_WARP_MAX) then thread-per-prime strikes
+// warp-cooperative strikes (p < P_WARP_MAX) then thread-per-prime strikes.
+// OffsetFn::small(i, p) / OffsetFn::large(i, p): window cell of the first
+// odd multiple of p >= max(p^2, q_w), or >= W when p misses the window.
 template <class OffsetFn>
 __device__ __forceinline__ void strike_primes(uint32_t* tile, const uint32_t* __restrict__ primes,
                                               uint32_t iA0, uint32_t iA1, uint32_t iB1,
-                                              OffsetFn off_of) {
+                                              const OffsetFn& off_of) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const uint32_t nwarps = blockDim.x >> 5;
     for (uint32_t i = iA0 + warp; i < iA1; i += nwarps) {
         uint32_t p = primes[i];
-        uint32_t off = off_of(i, p, false);
+        uint32_t off = off_of.small(i, p);
         if (off >= W) continue;
         uint32_t c = off + lane * p;
         const uint32_t step = 32 * p;
@@ -151,8 +153,8 @@ __device__ __forceinline__ void strike_primes(uint32_t* tile, const uint32_t* __
         }
     }
     for (uint32_t i = iA1 + threadIdx.x; i < iB1; i += blockDim.x) {
-        uint32_t p = primes[i];
-        uint32_t c = off_of(i, p, true);
+        uint32_t p = __ldg(primes + i);
+        uint32_t c = off_of.large(i, p);
         while (c < W) {
             strike(tile, c);
             c += p;
@@ -163,10 +165,11 @@ __device__ __forceinline__ void strike_primes(uint32_t* tile, const uint32_t* __
 // Generic window offset from a 64-bit window start (K1 / interval sieve).
 struct DirectOffset {
     uint64_t q_w;
-    __device__ __forceinline__ uint32_t operator()(uint32_t, uint32_t p, bool) const {
+    __device__ __forceinline__ uint32_t small(uint32_t, uint32_t p) const {
         uint64_t c = first_cell_u64(q_w, p);
         return c < W ? (uint32_t)c : W;
     }
+    __device__ __forceinline__ uint32_t large(uint32_t i, uint32_t p) const { return small(i, p); }
 };
 
 // Sieve-only kernel: bits of odd [lo, hi] into out (cell i <-> lo + 2i),
@@ -331,24 +334,27 @@ struct SegOffset {
     uint32_t iA0;
     uint32_t B;          // block start cell relative to qbase
     bool low;            // window starts at q = 1
-    __device__ __forceinline__ uint32_t operator()(uint32_t i, uint32_t p, bool fp) const {
-        if (low) {
-            uint64_t pp = (uint64_t)p * p;
-            uint64_t c = (pp - 1) >> 1;
-            return c < W ? (uint32_t)c : W;
-        }
-        uint32_t c = c0[i - iA0];
-        if (c >= B) {
-            uint32_t d = c - B;
-            return d < W ? d : W;
-        }
-        uint32_t x = B - c;
-        uint32_t r = fp ? mod_fp(x, p, __frcp_rn((float)p)) : x % p;
+    __device__ __forceinline__ uint32_t low_off(uint32_t p) const {
+        uint64_t c = ((uint64_t)p * p - 1) >> 1;
+        return c < W ? (uint32_t)c : W;
+    }
+    // p < 1024: integer remainder (warp-uniform, ~170 primes per block)
+    __device__ __forceinline__ uint32_t small(uint32_t i, uint32_t p) const {
+        if (low) return low_off(p);
+        uint32_t c = __ldg(c0 + (i - iA0));
+        if (c >= B) return min(c - B, W);
+        uint32_t r = (B - c) % p;
+        return r ? p - r : 0;
+    }
+    // p >= 1024: fp32 reciprocal remainder
+    __device__ __forceinline__ uint32_t large(uint32_t i, uint32_t p) const {
+        if (low) return low_off(p);
+        uint32_t c = __ldg(c0 + (i - iA0));
+        if (c >= B) return min(c - B, W);
+        uint32_t r = mod_fp(B - c, p, __fdividef(1.0f, (float)p));
         return r ? p - r : 0;
     }
 };
-
-
 
 __device__ __forceinline__ uint64_t window_bits(const uint32_t* tile, int64_t x) {
     // 64 cells [x-64, x) as a u64 (bit 63 <-> cell x-1); cells < 0 read as 0
@@ -365,6 +371,43 @@ __device__ __forceinline__ uint64_t window_bits(const uint32_t* tile, int64_t x)
     return v << (64 - x);
 }
 
+// Windows k >= 1 for one queued even of a fast block (il = block index);
+// not found in-tile -> straggler list.  Tie-aware max (queue order is not
+// the even order).
+template <bool PMIN>
+__device__ __forceinline__ void hard_windows(const uint32_t* tile, const uint64_t* pmr, uint32_t il, uint32_t i0,
+                                             uint32_t s, const SegJob& J, const VerifyArgs& A,
+                                             uint32_t jlim_small, uint32_t& sp, uint64_t& spi, uint32_t& mp,
+                                             uint32_t& mi) {
+    const int64_t x0 = (int64_t)JH + il + 1;
+    uint32_t p = 0;
+    for (uint32_t k = 1; k < (uint32_t)NWIN; ++k) {
+        uint64_t m = window_bits(tile, x0 - 64 * (int64_t)k) & pmr[k];
+        if (m) {
+            p = 3 + 2 * (64 * k + __clzll(m));
+            break;
+        }
+    }
+    const uint32_t iseg = i0 + il;
+    if (p) {
+        sp += p;
+        spi += (uint64_t)p * il;
+        if (p > mp || (p == mp && il < mi)) {
+            mp = p;
+            mi = il;
+        }
+    } else {
+        const uint64_t n = J.a + 2ull * iseg;
+        const uint64_t jq = (n - 6) >> 1;
+        const uint64_t jmax = jq < jlim_small ? jq : jlim_small;
+        const uint32_t flags = (uint64_t)JH <= jmax ? F_NEED_P1 : F_P1_FAIL;
+        unsigned idx = atomicAdd(A.list_count, 1u);
+        if (idx < A.list_cap) A.list[idx] = StragEntry{s, iseg, (uint32_t)JH, flags};
+    }
+    if constexpr (PMIN) A.pmin_out[iseg] = p;
+}
+
+template <bool PMIN>
 __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t* tile = smem;                                  // TILE_WORDS + pad
@@ -372,6 +415,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
     uint64_t* pmr = (uint64_t*)(smem + VERIFY_PMR_OFF);     // NWIN
     __shared__ uint32_t s_blk;
     __shared__ unsigned long long s_red[NWARPS][3];
+    __shared__ uint32_t s_hq[NWARPS][96]; // per-warp queue of evens needing windows k >= 1
 
     for (uint32_t i = threadIdx.x; i < PAT_WORDS; i += blockDim.x) pat[i] = A.gpat[i];
     for (uint32_t i = threadIdx.x; i < (uint32_t)NWIN; i += blockDim.x) pmr[i] = A.pmr[i];
@@ -411,29 +455,82 @@ __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
         // ---- K3: minimal p per even, while the tile is in shared memory
         const uint32_t i0 = b * E;
         const uint32_t ne = min(E, J.evens - i0);
-        // top cell of the block's first even: n - 3 - q_w over 2
-        const uint32_t t0 = low ? (uint32_t)((J.a - 4) >> 1) : (uint32_t)JH;
-        uint64_t sp = 0, spi = 0, key = 0;
-        for (uint32_t base = warp * 32; base < ne; base += blockDim.x) {
-            const uint32_t il = base + lane;
-            if (il < ne) {
+        const uint64_t n_first = J.a + 2ull * i0, n_last = n_first + 2ull * (ne - 1);
+        const bool inject_here = (A.inject & 1) == 0 && A.inject >= n_first && A.inject <= n_last;
+        // fast blocks: every even has all NWIN windows valid (n >= 8196,
+        // p_small >= 8193), no n = 4, no injected even
+        const bool fast = !low && jlim_small >= (uint32_t)JH - 1 && !inject_here;
+        uint32_t sp = 0, mp = 0, mi = 0xFFFFFFFFu; // Σp, max p and its block index
+        uint64_t spi = 0;                          // Σ p * il
+        if (fast) {
+            const uint32_t pm_lo = (uint32_t)pmr[0], pm_hi = (uint32_t)(pmr[0] >> 32);
+            uint32_t* q = s_hq[warp];
+            uint32_t qn = 0; // warp-uniform queue length
+            // each lane takes two consecutive evens il, il+1: their 64-cell
+            // windows [JH+il-63, JH+il] and one cell up fit in three words
+            for (uint32_t base = warp * 64; base < ne; base += 2 * blockDim.x) {
+                const uint32_t il = base + 2 * lane;
+                const bool va = il < ne, vb = il + 1 < ne;
+                const uint32_t lo = il + (JH - 63);
+                const uint32_t wi = lo >> 5, sh = lo & 31;
+                const uint32_t w0 = tile[wi], w1 = tile[wi + 1], w2 = tile[wi + 2];
+                const uint32_t la = __funnelshift_r(w0, w1, sh) & pm_lo;
+                const uint32_t ha = __funnelshift_r(w1, w2, sh) & pm_hi;
+                const uint32_t lb = __funnelshift_rc(w0, w1, sh + 1) & pm_lo;
+                const uint32_t hb = __funnelshift_rc(w1, w2, sh + 1) & pm_hi;
+                const bool fa = va && (ha | la) != 0;
+                const bool fb = vb && (hb | lb) != 0;
+                const uint32_t pa = fa ? 3 + 2 * (ha ? __clz(ha) : 32 + __clz(la)) : 0;
+                const uint32_t pb = fb ? 3 + 2 * (hb ? __clz(hb) : 32 + __clz(lb)) : 0;
+                sp += pa + pb;
+                spi += (uint64_t)pa * il + (uint64_t)pb * (il + 1);
+                // strict >: this lane's evens arrive in increasing order
+                if (pa > mp) { mp = pa; mi = il; }
+                if (pb > mp) { mp = pb; mi = il + 1; }
+                if constexpr (PMIN) {
+                    if (va) A.pmin_out[i0 + il] = pa;
+                    if (vb) A.pmin_out[i0 + il + 1] = pb;
+                }
+                const uint32_t ha_m = __ballot_sync(0xffffffffu, va && !fa);
+                const uint32_t hb_m = __ballot_sync(0xffffffffu, vb && !fb);
+                if (ha_m | hb_m) {
+                    const uint32_t below = (1u << lane) - 1;
+                    const uint32_t na = __popc(ha_m);
+                    if (va && !fa) q[qn + __popc(ha_m & below)] = il;
+                    if (vb && !fb) q[qn + na + __popc(hb_m & below)] = il + 1;
+                    qn += na + __popc(hb_m);
+                    __syncwarp();
+                    while (qn >= 32) {
+                        hard_windows<PMIN>(tile, pmr, q[qn - 32 + lane], i0, s, J, A, jlim_small, sp, spi, mp, mi);
+                        qn -= 32;
+                    }
+                    __syncwarp();
+                }
+            }
+            if (lane < qn) hard_windows<PMIN>(tile, pmr, q[lane], i0, s, J, A, jlim_small, sp, spi, mp, mi);
+            __syncwarp();
+        } else {
+            // generic path: low window (n = 4, q >= 3 limits), small p_small,
+            // injected even
+            const uint32_t t0 = low ? (uint32_t)((J.a - 4) >> 1) : (uint32_t)JH;
+            for (uint32_t base = warp * 32; base < ne; base += blockDim.x) {
+                const uint32_t il = base + lane;
+                if (il >= ne) continue;
                 const uint32_t iseg = i0 + il;
                 const uint64_t n = J.a + 2ull * iseg;
-                uint64_t p = 0;
+                uint32_t p = 0;
                 if (n == 4) {
                     p = 2;
                 } else {
                     const int64_t t = (int64_t)t0 + il;
-                    // candidates j <= jmax: p <= p_small, q >= 3, in-tile
                     const uint64_t jq = (n - 6) >> 1;
                     uint32_t jmax = jlim_small;
                     if (jq < jmax) jmax = (uint32_t)jq;
                     const uint32_t kmax = min((uint32_t)NWIN, jmax / 64 + 1);
-                    uint32_t k = 0;
-                    for (; k < kmax; ++k) {
+                    for (uint32_t k = 0; k < kmax; ++k) {
                         uint64_t m = window_bits(tile, t + 1 - 64 * (int64_t)k) & pmr[k];
                         if (m) {
-                            p = 3 + 2 * (64ull * k + __clzll(m));
+                            p = 3 + 2 * (64 * k + __clzll(m));
                             break;
                         }
                     }
@@ -449,26 +546,32 @@ __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
                 }
                 if (p) {
                     sp += p;
-                    spi += p * (uint64_t)iseg;
-                    uint64_t kk = (p << 32) | (0xFFFFFFFFu - iseg);
-                    key = kk > key ? kk : key;
+                    spi += (uint64_t)p * il;
+                    if (p > mp || (p == mp && il < mi)) {
+                        mp = p;
+                        mi = il;
+                    }
                     if (n == A.inject) {
                         unsigned idx = atomicAdd(A.list_count, 1u);
                         if (idx < A.list_cap) A.list[idx] = StragEntry{s, iseg, 0u, F_INJECT | F_OBSERVED};
                     }
                 }
-                if (A.pmin_out) A.pmin_out[iseg] = p;
+                if constexpr (PMIN) A.pmin_out[iseg] = p;
             }
         }
+        // per-thread -> Σp·iseg = Σp·il + i0·Σp; key = p << 32 | ~iseg
+        spi += (uint64_t)i0 * sp;
+        uint64_t key = mp ? (((uint64_t)mp << 32) | (0xFFFFFFFFu - (i0 + mi))) : 0;
+        uint64_t sp64 = sp;
         // ---- block reduction -> slot accumulators
         for (int o = 16; o; o >>= 1) {
-            sp += __shfl_xor_sync(0xffffffffu, sp, o);
+            sp64 += __shfl_xor_sync(0xffffffffu, sp64, o);
             spi += __shfl_xor_sync(0xffffffffu, spi, o);
             uint64_t ok = __shfl_xor_sync(0xffffffffu, key, o);
             key = ok > key ? ok : key;
         }
         if (lane == 0) {
-            s_red[warp][0] = sp;
+            s_red[warp][0] = sp64;
             s_red[warp][1] = spi;
             s_red[warp][2] = key;
         }
@@ -676,7 +779,10 @@ cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint3
     return cudaGetLastError();
 }
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st) {
-    k_verify_blocks<<<grid, THREADS, VERIFY_SMEM, st>>>(a);
+    if (a.pmin_out)
+        k_verify_blocks<true><<<grid, THREADS, VERIFY_SMEM, st>>>(a);
+    else
+        k_verify_blocks<false><<<grid, THREADS, VERIFY_SMEM, st>>>(a);
     return cudaGetLastError();
 }
 cudaError_t launch_stragglers(const SegJob* jobs, const StragEntry* list, const unsigned int* list_count,
@@ -703,13 +809,16 @@ cudaError_t launch_is_prime_batch(const uint64_t* v, uint8_t* out, uint64_t n, c
 }
 int verify_occupancy(int* blocks_per_sm) {
     // per-device function attributes: call after cudaSetDevice
-    if (cudaFuncSetAttribute(k_verify_blocks, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)VERIFY_SMEM) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(k_verify_blocks<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)VERIFY_SMEM) != cudaSuccess)
+        return 1;
+    if (cudaFuncSetAttribute(k_verify_blocks<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)VERIFY_SMEM) != cudaSuccess)
         return 1;
     if (cudaFuncSetAttribute(k_sieve_interval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SIEVE_SMEM) !=
         cudaSuccess)
         return 1;
-    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_verify_blocks, THREADS,
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_verify_blocks<false>, THREADS,
                                                               VERIFY_SMEM);
 }
 
