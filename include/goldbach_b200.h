@@ -191,6 +191,16 @@ int gb_flush_l2(gb_dev* dev);
 /* cudaDeviceSynchronize on the handle's device. */
 int gb_synchronize(gb_dev* dev);
 
+/* Device-clock interval timer (CUDA events): op 0 drains the device and
+ * records the start event; op 1 drains the device, records the stop event
+ * and writes the elapsed milliseconds to *ms.  Used by bench.py. */
+int gb_device_timer(gb_dev* dev, int op, double* ms);
+
+/* Measured shared-memory load bandwidth of the device in bytes/s
+ * (conflict-free 128-bit loads from 2 CTAs x 512 threads on every SM):
+ * the roofline denominator of the fused sieve+check kernel. */
+int gb_smem_peak(gb_dev* dev, double* bytes_per_s);
+
 #ifdef __cplusplus
 }
 #endif

@@ -143,6 +143,8 @@ def lib():
         "gb_flush_l2": ([vp], i32),
         "gb_synchronize": ([vp], i32),
         "gb_primes_upto": ([vp, u64, C.POINTER(C.c_uint32), u64, p64], i32),
+        "gb_device_timer": ([vp, i32, C.POINTER(C.c_double)], i32),
+        "gb_smem_peak": ([vp, C.POINTER(C.c_double)], i32),
     }
     for name, (args, res) in sig.items():
         fn = getattr(L, name)
@@ -325,6 +327,22 @@ class Device:
         _check(lib().gb_primes_upto(self._h, limit, out.ctypes.data_as(C.POINTER(C.c_uint32)),
                                     n.value, C.byref(n)), self._h)
         return out[: n.value]
+
+    def timer_start(self):
+        """Drain the device and record the start event (gb_device_timer)."""
+        _check(lib().gb_device_timer(self._h, 0, None), self._h)
+
+    def timer_stop(self) -> float:
+        """Drain the device, record the stop event; elapsed device ms."""
+        ms = C.c_double()
+        _check(lib().gb_device_timer(self._h, 1, C.byref(ms)), self._h)
+        return ms.value
+
+    def smem_peak(self) -> float:
+        """Measured shared-memory load bandwidth, bytes/s."""
+        v = C.c_double()
+        _check(lib().gb_smem_peak(self._h, C.byref(v)), self._h)
+        return v.value
 
     def kernel_times(self, reset: bool = False):
         ms = (C.c_double * 4)()

@@ -111,6 +111,9 @@ struct gb_dev {
     double kms[4] = {0, 0, 0, 0};
     uint64_t kl[4] = {0, 0, 0, 0};
     Batch sync;                    // private batch for the synchronous helpers
+    cudaEvent_t tm0 = nullptr, tm1 = nullptr; // gb_device_timer
+    cudaEvent_t t_ref = nullptr;   // timing origin (gb_set_timing)
+    double last_k1 = 0;            // end of the last fused launch, ms after t_ref
 };
 
 #define GB_FAIL(dev, code, msg)                      \
@@ -327,8 +330,15 @@ static int batch_complete(gb_dev* d, int bi) {
             d->kms[1] += ms;
             d->kl[1] += 1;
         }
-        if (cudaEventElapsedTime(&ms, b.ev_k0, b.ev_k1) == cudaSuccess) {
-            d->kms[0] += ms;
+        // fused kernel: time from max(own start, previous fused launch's end)
+        // to its end, so overlapping launches of consecutive batches are
+        // not double counted (their union is the time the kernel runs)
+        float t0 = 0, t1 = 0;
+        if (cudaEventElapsedTime(&t0, d->t_ref, b.ev_k0) == cudaSuccess &&
+            cudaEventElapsedTime(&t1, d->t_ref, b.ev_k1) == cudaSuccess) {
+            const double start = std::max<double>(t0, d->last_k1);
+            if (t1 > start) d->kms[0] += t1 - start;
+            d->last_k1 = std::max<double>(d->last_k1, t1);
             d->kl[0] += 1;
         }
         if (cudaEventElapsedTime(&ms, b.ev_k1, b.ev_s1) == cudaSuccess) {
@@ -562,6 +572,9 @@ int gb_close(gb_dev* d) {
     cudaDeviceSynchronize();
     for (auto& b : d->batches) batch_free(b);
     batch_free(d->sync);
+    if (d->tm0) cudaEventDestroy(d->tm0);
+    if (d->tm1) cudaEventDestroy(d->tm1);
+    if (d->t_ref) cudaEventDestroy(d->t_ref);
     cudaFree(d->d_primes);
     cudaFree(d->flush_buf);
     cudaFree(d->d_pat);
@@ -811,6 +824,14 @@ int gb_set_timing(gb_dev* d, int enabled) {
     if (!d->segs.empty()) GB_FAIL(d, GB_ERR_PARAM, "gb_set_timing: segments pending");
     d->timing = enabled != 0;
     d->serial = enabled == 2;
+    if (d->timing) {
+        CU(d, cudaSetDevice(d->device));
+        if (!d->t_ref) CU(d, cudaEventCreate(&d->t_ref));
+        CU(d, cudaDeviceSynchronize());
+        CU(d, cudaEventRecord(d->t_ref, d->sync.st));
+        CU(d, cudaEventSynchronize(d->t_ref));
+        d->last_k1 = 0;
+    }
     return GB_OK;
 }
 
@@ -835,6 +856,59 @@ int gb_synchronize(gb_dev* d) {
     if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
     CU(d, cudaSetDevice(d->device));
     CU(d, cudaDeviceSynchronize());
+    return GB_OK;
+}
+
+int gb_device_timer(gb_dev* d, int op, double* ms) {
+    if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
+    CU(d, cudaSetDevice(d->device));
+    if (!d->tm0) CU(d, cudaEventCreate(&d->tm0));
+    if (!d->tm1) CU(d, cudaEventCreate(&d->tm1));
+    // the device is drained on both sides, so the event pair on the private
+    // stream brackets every stream's work in between
+    CU(d, cudaDeviceSynchronize());
+    if (op == 0) {
+        CU(d, cudaEventRecord(d->tm0, d->sync.st));
+        CU(d, cudaEventSynchronize(d->tm0));
+        return GB_OK;
+    }
+    if (op != 1) GB_FAIL(d, GB_ERR_PARAM, "gb_device_timer: op must be 0 or 1");
+    CU(d, cudaEventRecord(d->tm1, d->sync.st));
+    CU(d, cudaEventSynchronize(d->tm1));
+    float e = 0;
+    CU(d, cudaEventElapsedTime(&e, d->tm0, d->tm1));
+    if (ms) *ms = e;
+    return GB_OK;
+}
+
+int gb_smem_peak(gb_dev* d, double* bytes_per_s) {
+    if (!d || !bytes_per_s) GB_FAIL(d, GB_ERR_PARAM, "gb_smem_peak: null argument");
+    CU(d, cudaSetDevice(d->device));
+    cudaStream_t st = d->sync.st;
+    uint32_t* sink = nullptr;
+    CU(d, cudaMalloc(&sink, 4096 * 4));
+    cudaEvent_t e0, e1;
+    CU(d, cudaEventCreate(&e0));
+    CU(d, cudaEventCreate(&e1));
+    const int grid = d->sms * 2;
+    const uint32_t iters = 1u << 14;
+    CU(d, launch_smem_peak(64, sink, grid, st)); // warm-up
+    double best = 0;
+    for (int rep = 0; rep < 3; ++rep) {
+        CU(d, cudaEventRecord(e0, st));
+        CU(d, launch_smem_peak(iters, sink, grid, st));
+        CU(d, cudaEventRecord(e1, st));
+        CU(d, cudaEventSynchronize(e1));
+        float ms = 0;
+        CU(d, cudaEventElapsedTime(&ms, e0, e1));
+        const double bytes = (double)grid * THREADS * iters * 8 * 16;
+        best = std::max(best, bytes / (ms * 1e-3));
+    }
+    d->launches += 4;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    cudaFree(sink);
+    *bytes_per_s = best;
     return GB_OK;
 }
 

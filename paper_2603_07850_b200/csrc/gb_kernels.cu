@@ -732,7 +732,40 @@ __global__ void k_finalize(const SegJob* __restrict__ jobs, uint32_t nslots, con
     }
 }
 
+// ============================================================ smem peak
+// Conflict-free 128-bit shared-memory loads from every resident warp: the
+// measured roofline denominator of the fused kernel (128 B/clk/SM nominal).
+__global__ void __launch_bounds__(THREADS, 2) k_smem_peak(uint32_t iters, uint32_t* sink) {
+    extern __shared__ __align__(16) uint4 sbuf[]; // 64 KiB
+    constexpr uint32_t N = 4096;
+    for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) sbuf[i] = make_uint4(i, i * 3, i * 5, i * 7);
+    __syncthreads();
+    uint32_t x = 0, y = 0, z = 0, w = 0;
+    const uint32_t idx = threadIdx.x;
+    for (uint32_t it = 0; it < iters; ++it) {
+#pragma unroll 8
+        for (uint32_t u = 0; u < 8; ++u) {
+            // warp-uniform offset, consecutive lanes: conflict-free
+            const uint4 v = sbuf[(idx + (it * 8 + u) * 32) & (N - 1)];
+            x ^= v.x;
+            y += v.y;
+            z ^= v.z;
+            w += v.w;
+        }
+    }
+    if ((x ^ y ^ z ^ w) == 0x9e3779b9u) sink[blockIdx.x] = x; // keep the loads
+}
+
 // ============================================================ launchers
+cudaError_t launch_smem_peak(uint32_t iters, uint32_t* sink, int grid, cudaStream_t st) {
+    static bool attr = false;
+    if (!attr) {
+        cudaFuncSetAttribute(k_smem_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
+        attr = true;
+    }
+    k_smem_peak<<<grid, THREADS, 65536, st>>>(iters, sink);
+    return cudaGetLastError();
+}
 cudaError_t launch_init_tables(uint32_t* pat, uint64_t* pmr, uint64_t p_small, cudaStream_t st) {
     k_init_tables<<<64, 256, 0, st>>>(pat, pmr, p_small);
     return cudaGetLastError();

@@ -75,6 +75,7 @@ cudaError_t launch_finalize(const SegJob* jobs, uint32_t nslots, const SlotAcc* 
                             DevRecord* out, cudaStream_t st);
 cudaError_t launch_phase2_one(uint64_t n, uint64_t* out, cudaStream_t st);
 cudaError_t launch_is_prime_batch(const uint64_t* v, uint8_t* out, uint64_t n, cudaStream_t st);
+cudaError_t launch_smem_peak(uint32_t iters, uint32_t* sink, int grid, cudaStream_t st);
 int verify_occupancy(int* blocks_per_sm);
 
 } // namespace gbk
