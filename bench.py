@@ -362,7 +362,9 @@ def main():
     peak_gbs = smem_peak / 1e9
     prof = load_json(os.path.join(ROOT, "profiles", "ncu_verify_summary.json")) or {}
     prof_w = prof.get(str(args.limit)) or {}
-    traffic = prof_w.get("dram_bytes_per_launch")
+    # DRAM bytes of the captured launch, scaled per even to this run's launches
+    per_even = prof_w.get("dram_bytes_per_even")
+    traffic = per_even * evens_timed_rank / max(verify_launches, 1) if per_even else None
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
     roofline = {
         "bound": "smem", "kernel": "k_verify_blocks (fused K2 sieve + K3 check)",
