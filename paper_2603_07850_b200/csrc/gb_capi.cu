@@ -19,6 +19,7 @@
 #include <string>
 #include <vector>
 
+#include "gb_arena.h"
 #include "gb_kernels.h"
 
 using namespace gbk;
@@ -96,6 +97,7 @@ struct gb_dev {
     uint64_t iL0 = 0, iL1 = 0;          // large primes
     uint32_t* d_pat = nullptr;
     uint64_t* d_pmr = nullptr;
+    uint2* d_pm = nullptr;              // {p, magic} of primes [iA1, iB1)
     uint64_t max_piece = 0;
     uint64_t qg_stride = 0; // words per slot
     Batch batches[NBATCH];
@@ -140,16 +142,16 @@ static void set_err(gb_dev* d, const std::string& m) {
 static int batch_alloc(gb_dev* d, Batch& b, bool with_qg) {
     if (!b.st) CU(d, cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking));
     uint32_t np = d->iB1 - d->iA0;
-    CU(d, cudaMalloc(&b.d_jobs, SLOTS * sizeof(SegJob)));
-    CU(d, cudaMalloc(&b.d_c0, (size_t)SLOTS * std::max<uint32_t>(np, 1) * 4));
-    if (with_qg && d->iL1 > d->iL0) CU(d, cudaMalloc(&b.d_qg, (size_t)SLOTS * d->qg_stride * 4));
-    CU(d, cudaMalloc(&b.d_acc, SLOTS * sizeof(SlotAcc)));
-    CU(d, cudaMalloc(&b.d_list, (size_t)LIST_CAP * sizeof(StragEntry)));
-    CU(d, cudaMalloc(&b.d_counters, 4 * sizeof(unsigned int)));
-    CU(d, cudaMalloc(&b.d_res, (size_t)LIST_CAP * sizeof(StragResult)));
-    CU(d, cudaMalloc(&b.d_rec, SLOTS * sizeof(DevRecord)));
-    CU(d, cudaMallocHost(&b.h_jobs, SLOTS * sizeof(SegJob)));
-    CU(d, cudaMallocHost(&b.h_rec, SLOTS * sizeof(DevRecord)));
+    CU(d, dmalloc(d->device, &b.d_jobs, SLOTS * sizeof(SegJob)));
+    CU(d, dmalloc(d->device, &b.d_c0, (size_t)SLOTS * std::max<uint32_t>(np, 1) * 4));
+    if (with_qg && d->iL1 > d->iL0) CU(d, dmalloc(d->device, &b.d_qg, (size_t)SLOTS * d->qg_stride * 4));
+    CU(d, dmalloc(d->device, &b.d_acc, SLOTS * sizeof(SlotAcc)));
+    CU(d, dmalloc(d->device, &b.d_list, (size_t)LIST_CAP * sizeof(StragEntry)));
+    CU(d, dmalloc(d->device, &b.d_counters, 4 * sizeof(unsigned int)));
+    CU(d, dmalloc(d->device, &b.d_res, (size_t)LIST_CAP * sizeof(StragResult)));
+    CU(d, dmalloc(d->device, &b.d_rec, SLOTS * sizeof(DevRecord)));
+    CU(d, hmalloc(&b.h_jobs, SLOTS * sizeof(SegJob)));
+    CU(d, hmalloc(&b.h_rec, SLOTS * sizeof(DevRecord)));
     CU(d, cudaEventCreateWithFlags(&b.ev_done, cudaEventDisableTiming));
     CU(d, cudaEventCreate(&b.ev_k0));
     CU(d, cudaEventCreate(&b.ev_k1));
@@ -158,17 +160,17 @@ static int batch_alloc(gb_dev* d, Batch& b, bool with_qg) {
     return GB_OK;
 }
 
-static void batch_free(Batch& b) {
-    cudaFree(b.d_jobs);
-    cudaFree(b.d_c0);
-    cudaFree(b.d_qg);
-    cudaFree(b.d_acc);
-    cudaFree(b.d_list);
-    cudaFree(b.d_counters);
-    cudaFree(b.d_res);
-    cudaFree(b.d_rec);
-    cudaFreeHost(b.h_jobs);
-    cudaFreeHost(b.h_rec);
+static void batch_free(gb_dev* d, Batch& b) {
+    dfree(d->device, b.d_jobs);
+    dfree(d->device, b.d_c0);
+    dfree(d->device, b.d_qg);
+    dfree(d->device, b.d_acc);
+    dfree(d->device, b.d_list);
+    dfree(d->device, b.d_counters);
+    dfree(d->device, b.d_res);
+    dfree(d->device, b.d_rec);
+    hfree(b.h_jobs);
+    hfree(b.h_rec);
     if (b.ev_done) cudaEventDestroy(b.ev_done);
     if (b.ev_k0) cudaEventDestroy(b.ev_k0);
     if (b.ev_k1) cudaEventDestroy(b.ev_k1);
@@ -232,6 +234,7 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     A.iB1 = d->iB1;
     A.np = np;
     A.c0 = b.d_c0;
+    A.pm = d->d_pm;
     A.qg = large ? b.d_qg : nullptr;
     A.qg_stride_words = d->qg_stride;
     A.gpat = d->d_pat;
@@ -423,14 +426,14 @@ static int device_odd_primes_upto(gb_dev* d, uint64_t L, uint32_t** d_out, uint6
     *d_out = nullptr;
     *count = 0;
     if (L < 3) {
-        CU(d, cudaMalloc(d_out, 4));
+        CU(d, dmalloc(d->device, d_out, 4));
         return GB_OK;
     }
     uint32_t lim = (uint32_t)std::min<uint64_t>(isqrt_floor(L) + 1, 65536);
     if (lim < 3) lim = 3;
     uint32_t *d_seed = nullptr, *d_nseed = nullptr;
-    CU(d, cudaMalloc(&d_seed, 8192 * 4));
-    CU(d, cudaMalloc(&d_nseed, 4));
+    CU(d, dmalloc(d->device, &d_seed, 8192 * 4));
+    CU(d, dmalloc(d->device, &d_nseed, 4));
     CU(d, launch_seed_primes(lim, d_seed, d_nseed, st));
     uint32_t nseed = 0;
     CU(d, cudaMemcpyAsync(&nseed, d_nseed, 4, cudaMemcpyDeviceToHost, st));
@@ -442,38 +445,38 @@ static int device_odd_primes_upto(gb_dev* d, uint64_t L, uint32_t** d_out, uint6
     const uint64_t n_cells = (L - 3) / 2 + 1;
     const uint64_t n_words = (n_cells + 31) / 32;
     uint32_t* d_bits = nullptr;
-    CU(d, cudaMalloc(&d_bits, (n_words + 1) * 4));
+    CU(d, dmalloc(d->device, &d_bits, (n_words + 1) * 4));
     int grid = (int)std::min<uint64_t>((n_cells + W - 1) / W, (uint64_t)d->sms * 2);
     CU(d, launch_sieve_interval(3, n_cells, d_seed, sA0, sA1, nseed, d->d_pat, d_bits, grid, st));
     const uint32_t chunk = 4096;
     const uint64_t n_chunks = (n_words + chunk - 1) / chunk;
     uint32_t* d_counts = nullptr;
     uint64_t *d_off = nullptr, *d_total = nullptr;
-    CU(d, cudaMalloc(&d_counts, n_chunks * 4));
-    CU(d, cudaMalloc(&d_off, n_chunks * 8));
-    CU(d, cudaMalloc(&d_total, 8));
+    CU(d, dmalloc(d->device, &d_counts, n_chunks * 4));
+    CU(d, dmalloc(d->device, &d_off, n_chunks * 8));
+    CU(d, dmalloc(d->device, &d_total, 8));
     CU(d, launch_count_words(d_bits, n_words, chunk, d_counts, n_chunks, st));
     CU(d, launch_scan(d_counts, n_chunks, d_off, d_total, st));
     uint64_t total = 0;
     CU(d, cudaMemcpyAsync(&total, d_total, 8, cudaMemcpyDeviceToHost, st));
     CU(d, cudaStreamSynchronize(st));
-    CU(d, cudaMalloc(d_out, std::max<uint64_t>(total, 1) * 4));
+    CU(d, dmalloc(d->device, d_out, std::max<uint64_t>(total, 1) * 4));
     CU(d, launch_compact(d_bits, n_words, chunk, d_off, 3, *d_out, n_chunks, st));
     d->launches += 6;
     CU(d, cudaStreamSynchronize(st));
-    cudaFree(d_bits);
-    cudaFree(d_counts);
-    cudaFree(d_off);
-    cudaFree(d_total);
-    cudaFree(d_seed);
-    cudaFree(d_nseed);
+    dfree(d->device, d_bits);
+    dfree(d->device, d_counts);
+    dfree(d->device, d_off);
+    dfree(d->device, d_total);
+    dfree(d->device, d_seed);
+    dfree(d->device, d_nseed);
     *count = total;
     return GB_OK;
 }
 
 static int build_tables(gb_dev* d) {
-    CU(d, cudaMalloc(&d->d_pat, PAT_WORDS * 4));
-    CU(d, cudaMalloc(&d->d_pmr, NWIN * 8));
+    CU(d, dmalloc(d->device, &d->d_pat, PAT_WORDS * 4));
+    CU(d, dmalloc(d->device, &d->d_pmr, NWIN * 8));
     CU(d, launch_init_tables(d->d_pat, d->d_pmr, d->prm.p_small, d->sync.st));
     d->launches++;
     int rc = device_odd_primes_upto(d, d->sqrt_bound, &d->d_primes, &d->n_primes);
@@ -488,6 +491,11 @@ static int build_tables(gb_dev* d) {
     d->iB1 = (uint32_t)(std::upper_bound(hp.begin(), hp.end(), P_TILE_MAX) - hp.begin());
     d->iL0 = d->iB1;
     d->iL1 = total;
+    const uint32_t nm = d->iB1 > d->iA1 ? d->iB1 - d->iA1 : 0;
+    CU(d, dmalloc(d->device, &d->d_pm, std::max<uint32_t>(nm, 1) * sizeof(uint2)));
+    CU(d, launch_prime_magic(d->d_primes + d->iA1, nm, d->d_pm, d->sync.st));
+    CU(d, cudaStreamSynchronize(d->sync.st));
+    d->launches++;
     return GB_OK;
 }
 
@@ -570,15 +578,16 @@ int gb_close(gb_dev* d) {
     if (!d) return GB_OK;
     cudaSetDevice(d->device);
     cudaDeviceSynchronize();
-    for (auto& b : d->batches) batch_free(b);
-    batch_free(d->sync);
+    for (auto& b : d->batches) batch_free(d, b);
+    batch_free(d, d->sync);
     if (d->tm0) cudaEventDestroy(d->tm0);
     if (d->tm1) cudaEventDestroy(d->tm1);
     if (d->t_ref) cudaEventDestroy(d->t_ref);
-    cudaFree(d->d_primes);
-    cudaFree(d->flush_buf);
-    cudaFree(d->d_pat);
-    cudaFree(d->d_pmr);
+    dfree(d->device, d->d_primes);
+    dfree(d->device, d->flush_buf);
+    dfree(d->device, d->d_pat);
+    dfree(d->device, d->d_pmr);
+    dfree(d->device, d->d_pm);
     delete d;
     return GB_OK;
 }
@@ -689,7 +698,7 @@ int gb_sieve_interval(gb_dev* d, uint64_t lo, uint64_t hi, uint64_t* words, uint
     CU(d, cudaSetDevice(d->device));
     cudaStream_t st = d->sync.st;
     uint32_t* d_bits = nullptr;
-    CU(d, cudaMalloc(&d_bits, need * 8 + 8));
+    CU(d, dmalloc(d->device, &d_bits, need * 8 + 8));
     CU(d, cudaMemsetAsync(d_bits, 0, need * 8 + 8, st));
     int grid = (int)std::min<uint64_t>((n_cells + W - 1) / W, (uint64_t)d->sms * 2);
     // every base prime (p^2 beyond hi strikes nothing)
@@ -698,7 +707,7 @@ int gb_sieve_interval(gb_dev* d, uint64_t lo, uint64_t hi, uint64_t* words, uint
     d->launches++;
     CU(d, cudaMemcpyAsync(words, d_bits, need * 8, cudaMemcpyDeviceToHost, st));
     CU(d, cudaStreamSynchronize(st));
-    cudaFree(d_bits);
+    dfree(d->device, d_bits);
     return GB_OK;
 }
 
@@ -711,11 +720,11 @@ int gb_phase1_pmin(gb_dev* d, uint64_t a, uint64_t b, uint64_t* out, uint64_t n_
     if (n > LIST_CAP - 16) GB_FAIL(d, GB_ERR_PARAM, "gb_phase1_pmin: at most 2^20 evens per call");
     CU(d, cudaSetDevice(d->device));
     uint64_t* d_out = nullptr;
-    CU(d, cudaMalloc(&d_out, n * 8));
+    CU(d, dmalloc(d->device, &d_out, n * 8));
     DevRecord r;
     rc = run_piece_sync(d, a, b, &r, d_out);
     if (rc == GB_OK) CU(d, cudaMemcpy(out, d_out, n * 8, cudaMemcpyDeviceToHost));
-    cudaFree(d_out);
+    dfree(d->device, d_out);
     return rc;
 }
 
@@ -726,15 +735,15 @@ int gb_is_prime_batch(gb_dev* d, const uint64_t* values, uint8_t* out, uint64_t 
     cudaStream_t st = d->sync.st;
     uint64_t* dv = nullptr;
     uint8_t* dout = nullptr;
-    CU(d, cudaMalloc(&dv, count * 8));
-    CU(d, cudaMalloc(&dout, count));
+    CU(d, dmalloc(d->device, &dv, count * 8));
+    CU(d, dmalloc(d->device, &dout, count));
     CU(d, cudaMemcpyAsync(dv, values, count * 8, cudaMemcpyHostToDevice, st));
     CU(d, launch_is_prime_batch(dv, dout, count, st));
     d->launches++;
     CU(d, cudaMemcpyAsync(out, dout, count, cudaMemcpyDeviceToHost, st));
     CU(d, cudaStreamSynchronize(st));
-    cudaFree(dv);
-    cudaFree(dout);
+    dfree(d->device, dv);
+    dfree(d->device, dout);
     return GB_OK;
 }
 
@@ -744,12 +753,12 @@ int gb_phase2_resolve(gb_dev* d, uint64_t n, uint64_t* p) {
     CU(d, cudaSetDevice(d->device));
     cudaStream_t st = d->sync.st;
     uint64_t* dp = nullptr;
-    CU(d, cudaMalloc(&dp, 8));
+    CU(d, dmalloc(d->device, &dp, 8));
     CU(d, launch_phase2_one(n, dp, st));
     d->launches++;
     CU(d, cudaMemcpyAsync(p, dp, 8, cudaMemcpyDeviceToHost, st));
     CU(d, cudaStreamSynchronize(st));
-    cudaFree(dp);
+    dfree(d->device, dp);
     return GB_OK;
 }
 
@@ -766,7 +775,7 @@ int gb_primes_upto(gb_dev* d, uint64_t limit, uint32_t* out, uint64_t cap, uint6
         uint64_t m = std::min(cap, n);
         if (m) CU(d, cudaMemcpy(out, dp, m * 4, cudaMemcpyDeviceToHost));
     }
-    cudaFree(dp);
+    dfree(d->device, dp);
     return GB_OK;
 }
 
@@ -846,7 +855,7 @@ int gb_flush_l2(gb_dev* d) {
     if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
     CU(d, cudaSetDevice(d->device));
     const size_t bytes = 256ull << 20; // > 126 MB L2
-    if (!d->flush_buf) CU(d, cudaMalloc(&d->flush_buf, bytes));
+    if (!d->flush_buf) CU(d, dmalloc(d->device, &d->flush_buf, bytes));
     CU(d, cudaMemsetAsync(d->flush_buf, d->launches & 0xff, bytes, d->sync.st));
     CU(d, cudaStreamSynchronize(d->sync.st));
     return GB_OK;
@@ -886,7 +895,7 @@ int gb_smem_peak(gb_dev* d, double* bytes_per_s) {
     CU(d, cudaSetDevice(d->device));
     cudaStream_t st = d->sync.st;
     uint32_t* sink = nullptr;
-    CU(d, cudaMalloc(&sink, 4096 * 4));
+    CU(d, dmalloc(d->device, &sink, 4096 * 4));
     cudaEvent_t e0, e1;
     CU(d, cudaEventCreate(&e0));
     CU(d, cudaEventCreate(&e1));
@@ -907,7 +916,7 @@ int gb_smem_peak(gb_dev* d, double* bytes_per_s) {
     d->launches += 4;
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    cudaFree(sink);
+    dfree(d->device, sink);
     *bytes_per_s = best;
     return GB_OK;
 }

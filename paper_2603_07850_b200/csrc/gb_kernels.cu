@@ -129,7 +129,18 @@ __device__ __forceinline__ void presieve_fixup(uint32_t* tile, uint64_t q_w) {
 }
 
 __device__ __forceinline__ void strike(uint32_t* tile, uint32_t c) {
-    atomicAnd(&tile[c >> 5], ~(1u << (c & 31)));
+    // ~(1 << (c & 31)) as one rotate of 0xFFFFFFFE
+    atomicAnd(&tile[c >> 5], __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, c));
+}
+
+// strikes c, c + step, ... < W (two per trip)
+__device__ __forceinline__ void strike_run(uint32_t* tile, uint32_t c, uint32_t step) {
+    while (c + step < W) {
+        strike(tile, c);
+        strike(tile, c + step);
+        c += 2 * step;
+    }
+    if (c < W) strike(tile, c);
 }
 
 // warp-cooperative strikes (p < P_WARP_MAX) then thread-per-prime strikes.
@@ -145,20 +156,11 @@ __device__ __forceinline__ void strike_primes(uint32_t* tile, const uint32_t* __
         uint32_t p = primes[i];
         uint32_t off = off_of.small(i, p);
         if (off >= W) continue;
-        uint32_t c = off + lane * p;
-        const uint32_t step = 32 * p;
-        while (c < W) {
-            strike(tile, c);
-            c += step;
-        }
+        strike_run(tile, off + lane * p, 32 * p);
     }
     for (uint32_t i = iA1 + threadIdx.x; i < iB1; i += blockDim.x) {
         uint32_t p = __ldg(primes + i);
-        uint32_t c = off_of.large(i, p);
-        while (c < W) {
-            strike(tile, c);
-            c += p;
-        }
+        strike_run(tile, off_of.large(i, p), p);
     }
 }
 
@@ -330,8 +332,7 @@ __global__ void k_large_strike(const SegJob* __restrict__ jobs, uint32_t nslots,
 // ============================================================ K2 + K3
 // Offsets for the verify path from the per-segment c0 table.
 struct SegOffset {
-    const uint32_t* c0;  // this slot's c0 row (index i - iA0)
-    uint32_t iA0;
+    const uint32_t* c0;  // this slot's c0 row, biased so that c0[i] is prime i's entry
     uint32_t B;          // block start cell relative to qbase
     bool low;            // window starts at q = 1
     __device__ __forceinline__ uint32_t low_off(uint32_t p) const {
@@ -341,20 +342,43 @@ struct SegOffset {
     // p < 1024: integer remainder (warp-uniform, ~170 primes per block)
     __device__ __forceinline__ uint32_t small(uint32_t i, uint32_t p) const {
         if (low) return low_off(p);
-        uint32_t c = __ldg(c0 + (i - iA0));
+        uint32_t c = __ldg(c0 + i);
         if (c >= B) return min(c - B, W);
         uint32_t r = (B - c) % p;
         return r ? p - r : 0;
     }
-    // p >= 1024: fp32 reciprocal remainder
-    __device__ __forceinline__ uint32_t large(uint32_t i, uint32_t p) const {
+    // p >= 1024: remainder by the prime's magic m = floor(2^32 / p):
+    // q = umulhi(x, m) is floor(x/p) or one less, so one correction
+    __device__ __forceinline__ uint32_t large_m(uint32_t i, uint32_t p, uint32_t m) const {
         if (low) return low_off(p);
-        uint32_t c = __ldg(c0 + (i - iA0));
+        uint32_t c = __ldg(c0 + i);
         if (c >= B) return min(c - B, W);
-        uint32_t r = mod_fp(B - c, p, __fdividef(1.0f, (float)p));
+        const uint32_t x = B - c;
+        uint32_t r = x - __umulhi(x, m) * p;
+        if (r >= p) r -= p;
         return r ? p - r : 0;
     }
 };
+
+// K2 strikes of one verify block: warp-cooperative below P_WARP_MAX, one
+// thread per prime above (primes + magics interleaved as uint2 {p, m}).
+__device__ __forceinline__ void strike_verify(uint32_t* tile, const uint32_t* __restrict__ primes,
+                                              const uint2* __restrict__ pm, uint32_t iA0, uint32_t iA1,
+                                              uint32_t iB1, const SegOffset& off) {
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const uint32_t nwarps = blockDim.x >> 5;
+    for (uint32_t i = iA0 + warp; i < iA1; i += nwarps) {
+        const uint32_t p = primes[i];
+        const uint32_t o = off.small(i, p);
+        if (o >= W) continue;
+        strike_run(tile, o + lane * p, 32 * p);
+    }
+    const uint2* pmb = pm - iA1;
+    for (uint32_t i = iA1 + threadIdx.x; i < iB1; i += blockDim.x) {
+        const uint2 e = __ldg(pmb + i);
+        strike_run(tile, off.large_m(i, e.x, e.y), e.x);
+    }
+}
 
 __device__ __forceinline__ uint64_t window_bits(const uint32_t* tile, int64_t x) {
     // 64 cells [x-64, x) as a u64 (bit 63 <-> cell x-1); cells < 0 read as 0
@@ -371,41 +395,134 @@ __device__ __forceinline__ uint64_t window_bits(const uint32_t* tile, int64_t x)
     return v << (64 - x);
 }
 
-// Windows k >= 1 for one queued even of a fast block (il = block index);
-// not found in-tile -> straggler list.  Tie-aware max (queue order is not
-// the even order).
-template <bool PMIN>
-__device__ __forceinline__ void hard_windows(const uint32_t* tile, const uint64_t* pmr, uint32_t il, uint32_t i0,
-                                             uint32_t s, const SegJob& J, const VerifyArgs& A,
-                                             uint32_t jlim_small, uint32_t& sp, uint64_t& spi, uint32_t& mp,
-                                             uint32_t& mi) {
-    const int64_t x0 = (int64_t)JH + il + 1;
-    uint32_t p = 0;
-    for (uint32_t k = 1; k < (uint32_t)NWIN; ++k) {
-        uint64_t m = window_bits(tile, x0 - 64 * (int64_t)k) & pmr[k];
-        if (m) {
-            p = 3 + 2 * (64 * k + __clzll(m));
-            break;
-        }
-    }
-    const uint32_t iseg = i0 + il;
-    if (p) {
-        sp += p;
-        spi += (uint64_t)p * il;
+// ------------------------------------------------------------ K3 helpers
+// 64 cells [x-64, x) as a u64 (bit 63 <-> cell x-1), x >= 64.
+__device__ __forceinline__ uint64_t window_bits_hi(const uint32_t* tile, uint32_t x) {
+    const uint32_t lo = x - 64;
+    const uint32_t wi = lo >> 5, sh = lo & 31;
+    const uint32_t w0 = tile[wi], w1 = tile[wi + 1], w2 = tile[wi + 2];
+    return ((uint64_t)__funnelshift_r(w1, w2, sh) << 32) | __funnelshift_r(w0, w1, sh);
+}
+
+// Per-thread K3 accumulators of one block.  Sums wrap mod 2^64 (the hard
+// path subtracts the placeholder p = 131 the fast path counted).
+struct K3Acc {
+    uint64_t sp = 0;          // sum p
+    uint64_t spi = 0;         // sum p * il (il = even index within the block)
+    uint32_t mp = 0;          // exact max p over generic + hard evens
+    uint32_t mi = 0xFFFFFFFFu; // its smallest il
+    __device__ __forceinline__ void observe(uint32_t p, uint32_t il) {
         if (p > mp || (p == mp && il < mi)) {
             mp = p;
             mi = il;
         }
+    }
+};
+
+// Window-0 miss marker of the fast path: z = 64 <-> "p = 131".
+constexpr uint32_t P_HARD = 3 + 2 * 64;
+
+// Straggler entry for an even with no candidate inside the in-tile halo.
+__device__ __forceinline__ void push_straggler(const VerifyArgs& A, const SegJob& J, uint32_t s, uint32_t iseg,
+                                               uint32_t jlim_small, uint32_t extra_flags) {
+    const uint64_t n = J.a + 2ull * iseg;
+    const uint64_t jq = (n - 6) >> 1;
+    const uint64_t jmax = jq < jlim_small ? jq : jlim_small;
+    const uint32_t flags = ((uint64_t)JH <= jmax ? F_NEED_P1 : F_P1_FAIL) | extra_flags;
+    const unsigned idx = atomicAdd(A.list_count, 1u);
+    if (idx < A.list_cap) A.list[idx] = StragEntry{s, iseg, (uint32_t)JH, flags};
+}
+
+// Hard evens of a fast block (no candidate p <= 129): the fast path counted
+// each as the placeholder p = P_HARD.  found_hard replaces it by the true p
+// (>= 131) or removes it and hands the even to K4.  Queue order is not even
+// order, hence the tie-aware max.
+template <bool PMIN>
+__device__ __forceinline__ void found_hard(uint32_t p, uint32_t il, uint32_t i0, uint32_t s, const SegJob& J,
+                                           const VerifyArgs& A, uint32_t jlim_small, K3Acc& acc) {
+    const uint32_t iseg = i0 + il;
+    if (p) {
+        acc.sp += p - P_HARD;
+        acc.spi += (uint64_t)(p - P_HARD) * il;
+        acc.observe(p, il);
     } else {
-        const uint64_t n = J.a + 2ull * iseg;
-        const uint64_t jq = (n - 6) >> 1;
-        const uint64_t jmax = jq < jlim_small ? jq : jlim_small;
-        const uint32_t flags = (uint64_t)JH <= jmax ? F_NEED_P1 : F_P1_FAIL;
-        unsigned idx = atomicAdd(A.list_count, 1u);
-        if (idx < A.list_cap) A.list[idx] = StragEntry{s, iseg, (uint32_t)JH, flags};
+        acc.sp -= P_HARD;
+        acc.spi -= (uint64_t)P_HARD * il;
+        push_straggler(A, J, s, iseg, jlim_small, 0);
     }
     if constexpr (PMIN) A.pmin_out[iseg] = p;
 }
+
+// Level 2: windows k = 2 .. NWIN-1 of one even (one exit, p computed once).
+template <bool PMIN>
+__device__ __forceinline__ void deep_even(const uint32_t* tile, const uint64_t* pmr, uint32_t il, uint32_t i0,
+                                          uint32_t s, const SegJob& J, const VerifyArgs& A, uint32_t jlim_small,
+                                          K3Acc& acc) {
+    const uint32_t x0 = (uint32_t)JH + il + 1;
+    uint32_t k = 2;
+    uint64_t m = 0;
+#pragma unroll 1
+    for (; k < (uint32_t)NWIN; ++k) {
+        m = window_bits_hi(tile, x0 - 64 * k) & pmr[k];
+        if (m) break;
+    }
+    const uint32_t p = m ? 3 + 2 * (64 * k + __clzll(m)) : 0;
+    found_hard<PMIN>(p, il, i0, s, J, A, jlim_small, acc);
+}
+
+// Generic per-even check (low window, n = 4, q >= 3 limits, small p_small,
+// injected even, block tails): exact windows k < kmax.
+template <bool PMIN>
+__device__ __forceinline__ void generic_even(const uint32_t* tile, const uint64_t* pmr, uint32_t il, uint32_t t0,
+                                             uint32_t i0, uint32_t s, const SegJob& J, const VerifyArgs& A,
+                                             uint32_t jlim_small, K3Acc& acc) {
+    const uint32_t iseg = i0 + il;
+    const uint64_t n = J.a + 2ull * iseg;
+    uint32_t p = 0;
+    if (n == 4) {
+        p = 2;
+    } else {
+        const int64_t t = (int64_t)t0 + il;
+        const uint64_t jq = (n - 6) >> 1;
+        uint32_t jmax = jlim_small;
+        if (jq < jmax) jmax = (uint32_t)jq;
+        const uint32_t kmax = min((uint32_t)NWIN, jmax / 64 + 1);
+        for (uint32_t k = 0; k < kmax; ++k) {
+            const uint64_t m = window_bits(tile, t + 1 - 64 * (int64_t)k) & pmr[k];
+            if (m) {
+                p = 3 + 2 * (64 * k + __clzll(m));
+                break;
+            }
+        }
+        // a hit beyond jmax cannot occur: pmr caps p_small and cells below
+        // q = 3 are zero (low window) or absent
+        if (!p) push_straggler(A, J, s, iseg, jlim_small, n == A.inject ? F_INJECT : 0u);
+    }
+    if (p) {
+        acc.sp += p;
+        acc.spi += (uint64_t)p * il;
+        acc.observe(p, il);
+        if (n == A.inject) {
+            const unsigned idx = atomicAdd(A.list_count, 1u);
+            if (idx < A.list_cap) A.list[idx] = StragEntry{s, iseg, 0u, F_INJECT | F_OBSERVED};
+        }
+    }
+    if constexpr (PMIN) A.pmin_out[iseg] = p;
+}
+
+// z of the 64-candidate window 0 of one even: index of the smallest
+// candidate p = 3 + 2z with n - p prime, 64 if none (w0..w2 hold the cells
+// [lo - sh, lo - sh + 96), the window starts at cell lo - sh + sh_t).
+__device__ __forceinline__ uint32_t zwin0(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t sh_t, uint32_t pm_lo,
+                                          uint32_t pm_hi) {
+    const uint32_t l = __funnelshift_rc(w0, w1, sh_t) & pm_lo;
+    const uint32_t h = __funnelshift_rc(w1, w2, sh_t) & pm_hi;
+    return h ? __clz(h) : 32 + __clz(l);
+}
+
+constexpr uint32_t CHUNK = 128;            // evens per warp iteration (4 per lane)
+constexpr uint32_t HQ = 64;                // per-warp level-2 queue
+constexpr uint32_t FLUSH_IT = 4;           // fast iterations between hard-even flushes
 
 template <bool PMIN>
 __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
@@ -415,7 +532,9 @@ __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
     uint64_t* pmr = (uint64_t*)(smem + VERIFY_PMR_OFF);     // NWIN
     __shared__ uint32_t s_blk;
     __shared__ unsigned long long s_red[NWARPS][3];
-    __shared__ uint32_t s_hq[NWARPS][96]; // per-warp queue of evens needing windows k >= 1
+    __shared__ unsigned long long s_key;
+    __shared__ uint16_t s_q1[NWARPS][FLUSH_IT * CHUNK]; // level-1 hard-even queue (offsets from base0)
+    __shared__ uint32_t s_q2[NWARPS][HQ];        // level-2 queue (evens needing windows k >= 2)
 
     for (uint32_t i = threadIdx.x; i < PAT_WORDS; i += blockDim.x) pat[i] = A.gpat[i];
     for (uint32_t i = threadIdx.x; i < (uint32_t)NWIN; i += blockDim.x) pmr[i] = A.pmr[i];
@@ -442,8 +561,8 @@ __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
         presieve_window(tile, pat, q_w);
         __syncthreads();
         presieve_fixup(tile, q_w);
-        SegOffset off{A.c0 + (uint64_t)s * A.np, A.iA0, B, low};
-        strike_primes(tile, A.primes, A.iA0, A.iA1, A.iB1, off);
+        const SegOffset off{A.c0 + ((int64_t)s * A.np - (int64_t)A.iA0), B, low};
+        strike_verify(tile, A.primes, A.pm, A.iA0, A.iA1, A.iB1, off);
         __syncthreads();
         if (A.qg != nullptr && !low && J.qg_words) {
             const uint32_t* g = A.qg + s * A.qg_stride_words + B / 32;
@@ -460,114 +579,104 @@ __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
         // fast blocks: every even has all NWIN windows valid (n >= 8196,
         // p_small >= 8193), no n = 4, no injected even
         const bool fast = !low && jlim_small >= (uint32_t)JH - 1 && !inject_here;
-        uint32_t sp = 0, mp = 0, mi = 0xFFFFFFFFu; // Σp, max p and its block index
-        uint64_t spi = 0;                          // Σ p * il
+        K3Acc acc;
+        uint32_t nfull = 0;       // evens [0, nfull) went through the fast path
         if (fast) {
             const uint32_t pm_lo = (uint32_t)pmr[0], pm_hi = (uint32_t)(pmr[0] >> 32);
-            uint32_t* q = s_hq[warp];
-            uint32_t qn = 0; // warp-uniform queue length
-            // each lane takes two consecutive evens il, il+1: their 64-cell
-            // windows [JH+il-63, JH+il] and one cell up fit in three words
-            for (uint32_t base = warp * 64; base < ne; base += 2 * blockDim.x) {
-                const uint32_t il = base + 2 * lane;
-                const bool va = il < ne, vb = il + 1 < ne;
-                const uint32_t lo = il + (JH - 63);
-                const uint32_t wi = lo >> 5, sh = lo & 31;
-                const uint32_t w0 = tile[wi], w1 = tile[wi + 1], w2 = tile[wi + 2];
-                const uint32_t la = __funnelshift_r(w0, w1, sh) & pm_lo;
-                const uint32_t ha = __funnelshift_r(w1, w2, sh) & pm_hi;
-                const uint32_t lb = __funnelshift_rc(w0, w1, sh + 1) & pm_lo;
-                const uint32_t hb = __funnelshift_rc(w1, w2, sh + 1) & pm_hi;
-                const bool fa = va && (ha | la) != 0;
-                const bool fb = vb && (hb | lb) != 0;
-                const uint32_t pa = fa ? 3 + 2 * (ha ? __clz(ha) : 32 + __clz(la)) : 0;
-                const uint32_t pb = fb ? 3 + 2 * (hb ? __clz(hb) : 32 + __clz(lb)) : 0;
-                sp += pa + pb;
-                spi += (uint64_t)pa * il + (uint64_t)pb * (il + 1);
-                // strict >: this lane's evens arrive in increasing order
-                if (pa > mp) { mp = pa; mi = il; }
-                if (pb > mp) { mp = pb; mi = il + 1; }
-                if constexpr (PMIN) {
-                    if (va) A.pmin_out[i0 + il] = pa;
-                    if (vb) A.pmin_out[i0 + il + 1] = pb;
+            const uint64_t pm1 = pmr[1];
+            uint16_t* q1 = s_q1[warp];
+            uint32_t* q2 = s_q2[warp];
+            uint32_t q2n = 0;     // warp-uniform level-2 length (< 32 between batches)
+            nfull = ne & ~(CHUNK - 1);
+            uint32_t zs = 0, tz = 0, iters = 0;
+            uint64_t hp = 0;
+            uint32_t base = warp * CHUNK;
+            while (base < nfull) {
+                // up to FLUSH_IT iterations; hard evens collected as bits 4k + t
+                uint32_t hm = 0;
+                const uint32_t base0 = base;
+#pragma unroll 1
+                for (uint32_t k = 0; k < FLUSH_IT && base < nfull; ++k, base += CHUNK * NWARPS) {
+                    // lane owns evens il0..il0+3: their 64-cell windows
+                    // [JH+il0+t-63, JH+il0+t] lie in 3 words (sh <= 29)
+                    const uint32_t il0 = base + 4 * lane;
+                    const uint32_t lo = il0 + (JH - 63);
+                    const uint32_t wi = lo >> 5, sh = lo & 31;
+                    const uint32_t w0 = tile[wi], w1 = tile[wi + 1], w2 = tile[wi + 2];
+                    const uint32_t z0 = zwin0(w0, w1, w2, sh, pm_lo, pm_hi);
+                    const uint32_t z1 = zwin0(w0, w1, w2, sh + 1, pm_lo, pm_hi);
+                    const uint32_t z2 = zwin0(w0, w1, w2, sh + 2, pm_lo, pm_hi);
+                    const uint32_t z3 = zwin0(w0, w1, w2, sh + 3, pm_lo, pm_hi);
+                    const uint32_t zsum = z0 + z1 + z2 + z3;
+                    zs += zsum;
+                    tz += z1 + 2 * z2 + 3 * z3;
+                    hp += (uint64_t)(12 + 2 * zsum) * il0;
+                    hm |= ((z0 >> 6) | ((z1 >> 5) & 2u) | ((z2 >> 4) & 4u) | ((z3 >> 3) & 8u)) << (4 * k);
+                    ++iters;
+                    if constexpr (PMIN) {
+                        A.pmin_out[i0 + il0 + 0] = z0 < 64 ? 3 + 2 * z0 : 0;
+                        A.pmin_out[i0 + il0 + 1] = z1 < 64 ? 3 + 2 * z1 : 0;
+                        A.pmin_out[i0 + il0 + 2] = z2 < 64 ? 3 + 2 * z2 : 0;
+                        A.pmin_out[i0 + il0 + 3] = z3 < 64 ? 3 + 2 * z3 : 0;
+                    }
                 }
-                const uint32_t ha_m = __ballot_sync(0xffffffffu, va && !fa);
-                const uint32_t hb_m = __ballot_sync(0xffffffffu, vb && !fb);
-                if (ha_m | hb_m) {
-                    const uint32_t below = (1u << lane) - 1;
-                    const uint32_t na = __popc(ha_m);
-                    if (va && !fa) q[qn + __popc(ha_m & below)] = il;
-                    if (vb && !fb) q[qn + na + __popc(hb_m & below)] = il + 1;
-                    qn += na + __popc(hb_m);
+                // compact this lane's hard bits into the warp's level-1 queue
+                // (u16 offsets from base0) with one warp prefix sum
+                const uint32_t c = __popc(hm);
+                uint32_t incl = c;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= (uint32_t)o) incl += y;
+                }
+                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                uint32_t pos = incl - c;
+                while (hm) {
+                    const uint32_t bit = __ffs(hm) - 1;
+                    hm &= hm - 1;
+                    q1[pos++] = (uint16_t)((bit >> 2) * (CHUNK * NWARPS) + 4 * lane + (bit & 3));
+                }
+                __syncwarp();
+                // level 1: window k = 1 for 32 hard evens at a time; misses go
+                // to the level-2 queue, drained 32 at a time
+                for (uint32_t e0 = 0; e0 < total; e0 += 32) {
+                    const uint32_t e = e0 + lane;
+                    const bool act = e < total;
+                    const uint32_t il = base0 + (act ? (uint32_t)q1[e] : 0u);
+                    const uint64_t m = act ? window_bits_hi(tile, (uint32_t)JH + il + 1 - 64) & pm1 : 0;
+                    if (m) found_hard<PMIN>(3 + 2 * (64 + __clzll(m)), il, i0, s, J, A, jlim_small, acc);
+                    const bool miss = act && !m;
+                    const uint32_t bal = __ballot_sync(0xffffffffu, miss);
+                    if (miss) q2[q2n + __popc(bal & ((1u << lane) - 1))] = il;
+                    q2n += __popc(bal);
                     __syncwarp();
-                    while (qn >= 32) {
-                        hard_windows<PMIN>(tile, pmr, q[qn - 32 + lane], i0, s, J, A, jlim_small, sp, spi, mp, mi);
-                        qn -= 32;
+                    if (q2n >= 32) {
+                        deep_even<PMIN>(tile, pmr, q2[q2n - 32 + lane], i0, s, J, A, jlim_small, acc);
+                        q2n -= 32;
                     }
                     __syncwarp();
                 }
             }
-            if (lane < qn) hard_windows<PMIN>(tile, pmr, q[lane], i0, s, J, A, jlim_small, sp, spi, mp, mi);
+            if (lane < q2n) deep_even<PMIN>(tile, pmr, q2[lane], i0, s, J, A, jlim_small, acc);
             __syncwarp();
-        } else {
-            // generic path: low window (n = 4, q >= 3 limits), small p_small,
-            // injected even
-            const uint32_t t0 = low ? (uint32_t)((J.a - 4) >> 1) : (uint32_t)JH;
-            for (uint32_t base = warp * 32; base < ne; base += blockDim.x) {
-                const uint32_t il = base + lane;
-                if (il >= ne) continue;
-                const uint32_t iseg = i0 + il;
-                const uint64_t n = J.a + 2ull * iseg;
-                uint32_t p = 0;
-                if (n == 4) {
-                    p = 2;
-                } else {
-                    const int64_t t = (int64_t)t0 + il;
-                    const uint64_t jq = (n - 6) >> 1;
-                    uint32_t jmax = jlim_small;
-                    if (jq < jmax) jmax = (uint32_t)jq;
-                    const uint32_t kmax = min((uint32_t)NWIN, jmax / 64 + 1);
-                    for (uint32_t k = 0; k < kmax; ++k) {
-                        uint64_t m = window_bits(tile, t + 1 - 64 * (int64_t)k) & pmr[k];
-                        if (m) {
-                            p = 3 + 2 * (64 * k + __clzll(m));
-                            break;
-                        }
-                    }
-                    // a hit beyond jmax cannot occur: pmr caps p_small and
-                    // cells below q = 3 are zero (low window) or absent
-                    if (!p) {
-                        bool more = (uint64_t)JH <= jmax; // candidates beyond the halo remain
-                        uint32_t flags = more ? F_NEED_P1 : F_P1_FAIL;
-                        if (n == A.inject) flags |= F_INJECT;
-                        unsigned idx = atomicAdd(A.list_count, 1u);
-                        if (idx < A.list_cap) A.list[idx] = StragEntry{s, iseg, (uint32_t)JH, flags};
-                    }
-                }
-                if (p) {
-                    sp += p;
-                    spi += (uint64_t)p * il;
-                    if (p > mp || (p == mp && il < mi)) {
-                        mp = p;
-                        mi = il;
-                    }
-                    if (n == A.inject) {
-                        unsigned idx = atomicAdd(A.list_count, 1u);
-                        if (idx < A.list_cap) A.list[idx] = StragEntry{s, iseg, 0u, F_INJECT | F_OBSERVED};
-                    }
-                }
-                if constexpr (PMIN) A.pmin_out[iseg] = p;
-            }
+            // p_t = 3 + 2 z_t: sum p = 12 per iteration + 2 sum z; sum p*il =
+            // sum P4*il0 + sum (p1 + 2 p2 + 3 p3) = hp + 18 iters + 2 tz
+            acc.sp += 12ull * iters + 2ull * zs;
+            acc.spi += hp + 18ull * iters + 2ull * tz;
         }
-        // per-thread -> Σp·iseg = Σp·il + i0·Σp; key = p << 32 | ~iseg
-        spi += (uint64_t)i0 * sp;
-        uint64_t key = mp ? (((uint64_t)mp << 32) | (0xFFFFFFFFu - (i0 + mi))) : 0;
-        uint64_t sp64 = sp;
-        // ---- block reduction -> slot accumulators
+        {
+            // generic path (whole block, or the tail of a fast block)
+            const uint32_t t0 = low ? (uint32_t)((J.a - 4) >> 1) : (uint32_t)JH;
+            for (uint32_t il = nfull + threadIdx.x; il < ne; il += blockDim.x)
+                generic_even<PMIN>(tile, pmr, il, t0, i0, s, J, A, jlim_small, acc);
+        }
+        // ---- block reduction -> slot accumulators; key = p << 32 | ~iseg
+        uint64_t key = acc.mp ? (((uint64_t)acc.mp << 32) | (0xFFFFFFFFu - (i0 + acc.mi))) : 0;
+        uint64_t sp64 = acc.sp, spi = acc.spi + (uint64_t)i0 * acc.sp;
         for (int o = 16; o; o >>= 1) {
             sp64 += __shfl_xor_sync(0xffffffffu, sp64, o);
             spi += __shfl_xor_sync(0xffffffffu, spi, o);
-            uint64_t ok = __shfl_xor_sync(0xffffffffu, key, o);
+            const uint64_t ok = __shfl_xor_sync(0xffffffffu, key, o);
             key = ok > key ? ok : key;
         }
         if (lane == 0) {
@@ -585,8 +694,39 @@ __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
             }
             atomicAdd(&A.acc[s].sum, (unsigned long long)S);
             atomicAdd(&A.acc[s].hash, (unsigned long long)((J.a >> 1) * S + SPI));
-            if (K) atomicMax(&A.acc[s].key, (unsigned long long)K);
+            s_key = K;
         }
+        __syncthreads();
+        uint64_t K = s_key;
+        if (nfull && K < ((uint64_t)P_HARD << 32)) {
+            // no in-tile p >= 131: the block max may be a fast even, whose
+            // index the fast path did not keep -- rescan window 0 exactly
+            const uint32_t pm_lo = (uint32_t)pmr[0], pm_hi = (uint32_t)(pmr[0] >> 32);
+            uint32_t bz = 0, bi = 0xFFFFFFFFu;
+            for (uint32_t base = warp * CHUNK; base < nfull; base += CHUNK * NWARPS) {
+                const uint32_t il0 = base + 4 * lane;
+                const uint32_t lo = il0 + (JH - 63);
+                const uint32_t wi = lo >> 5, sh = lo & 31;
+                const uint32_t w0 = tile[wi], w1 = tile[wi + 1], w2 = tile[wi + 2];
+#pragma unroll
+                for (uint32_t t = 0; t < 4; ++t) {
+                    const uint32_t z = zwin0(w0, w1, w2, sh + t, pm_lo, pm_hi);
+                    if (z < 64 && (bi == 0xFFFFFFFFu || z > bz)) {
+                        bz = z;
+                        bi = il0 + t;
+                    }
+                }
+            }
+            uint64_t kf = bi != 0xFFFFFFFFu ? (((uint64_t)(3 + 2 * bz) << 32) | (0xFFFFFFFFu - (i0 + bi))) : 0;
+            for (int o = 16; o; o >>= 1) {
+                const uint64_t ok = __shfl_xor_sync(0xffffffffu, kf, o);
+                kf = ok > kf ? ok : kf;
+            }
+            if (lane == 0) atomicMax(&s_key, (unsigned long long)kf);
+            __syncthreads();
+            K = s_key;
+        }
+        if (threadIdx.x == 0 && K) atomicMax(&A.acc[s].key, (unsigned long long)K);
     }
 }
 
@@ -732,6 +872,14 @@ __global__ void k_finalize(const SegJob* __restrict__ jobs, uint32_t nslots, con
     }
 }
 
+// magic[i] = floor(2^32 / p) for the thread-per-prime tile primes, as {p, m}
+__global__ void k_prime_magic(const uint32_t* __restrict__ primes, uint32_t n, uint2* __restrict__ pm) {
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+        const uint32_t p = primes[i];
+        pm[i] = make_uint2(p, (uint32_t)((1ull << 32) / p));
+    }
+}
+
 // ============================================================ smem peak
 // Conflict-free 128-bit shared-memory loads from every resident warp: the
 // measured roofline denominator of the fused kernel (128 B/clk/SM nominal).
@@ -764,6 +912,11 @@ cudaError_t launch_smem_peak(uint32_t iters, uint32_t* sink, int grid, cudaStrea
         attr = true;
     }
     k_smem_peak<<<grid, THREADS, 65536, st>>>(iters, sink);
+    return cudaGetLastError();
+}
+cudaError_t launch_prime_magic(const uint32_t* primes, uint32_t n, uint2* pm, cudaStream_t st) {
+    if (!n) return cudaSuccess;
+    k_prime_magic<<<(n + 255) / 256, 256, 0, st>>>(primes, n, pm);
     return cudaGetLastError();
 }
 cudaError_t launch_init_tables(uint32_t* pat, uint64_t* pmr, uint64_t p_small, cudaStream_t st) {

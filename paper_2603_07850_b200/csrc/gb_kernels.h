@@ -29,6 +29,7 @@ struct VerifyArgs {
     uint32_t iA0, iA1, iB1;       // tile prime index ranges
     uint32_t np;                  // c0 row length (iB1 - iA0)
     const uint32_t* c0;           // nslots * np
+    const uint2* pm;              // {p, floor(2^32/p)} of primes [iA1, iB1)
     const uint32_t* qg;           // large-prime bitmask (nullptr = none)
     uint64_t qg_stride_words;
     const uint32_t* gpat;
@@ -75,6 +76,7 @@ cudaError_t launch_finalize(const SegJob* jobs, uint32_t nslots, const SlotAcc* 
                             DevRecord* out, cudaStream_t st);
 cudaError_t launch_phase2_one(uint64_t n, uint64_t* out, cudaStream_t st);
 cudaError_t launch_is_prime_batch(const uint64_t* v, uint8_t* out, uint64_t n, cudaStream_t st);
+cudaError_t launch_prime_magic(const uint32_t* primes, uint32_t n, uint2* pm, cudaStream_t st);
 cudaError_t launch_smem_peak(uint32_t iters, uint32_t* sink, int grid, cudaStream_t st);
 int verify_occupancy(int* blocks_per_sm);
 
