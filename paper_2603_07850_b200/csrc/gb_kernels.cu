@@ -17,6 +17,7 @@
 //       k_finalize         per-segment record (verify_segment's report,
 //                          verifier.cpp:167-206, + checksum)
 #include "gb_kernels.h"
+#include "gb_bitslice.cuh"
 
 #include <algorithm>
 #include <cstdio>
@@ -404,12 +405,11 @@ __device__ __forceinline__ uint64_t window_bits_hi(const uint32_t* tile, uint32_
     return ((uint64_t)__funnelshift_r(w1, w2, sh) << 32) | __funnelshift_r(w0, w1, sh);
 }
 
-// Per-thread K3 accumulators of one block.  Sums wrap mod 2^64 (the hard
-// path subtracts the placeholder p = 131 the fast path counted).
+// Per-thread K3 accumulators of one block (sums wrap mod 2^64).
 struct K3Acc {
     uint64_t sp = 0;          // sum p
     uint64_t spi = 0;         // sum p * il (il = even index within the block)
-    uint32_t mp = 0;          // exact max p over generic + hard evens
+    uint32_t mp = 0;          // max p over per-even (deep / generic) evens
     uint32_t mi = 0xFFFFFFFFu; // its smallest il
     __device__ __forceinline__ void observe(uint32_t p, uint32_t il) {
         if (p > mp || (p == mp && il < mi)) {
@@ -419,8 +419,12 @@ struct K3Acc {
     }
 };
 
-// Window-0 miss marker of the fast path: z = 64 <-> "p = 131".
-constexpr uint32_t P_HARD = 3 + 2 * 64;
+// Candidates z < ZBS (p <= 3 + 2(ZBS-1) = 257) are scanned bit-sliced, 32
+// evens per lane (gb_bitslice.cuh); the few evens left ("deep") continue
+// per even from window ZBS/64.
+constexpr uint32_t ZBS = 128;
+constexpr int NPL = BS_SCAN128_PLANES;   // z planes
+constexpr uint32_t QCAP = 160;           // per-warp deep-even queue
 
 // Straggler entry for an even with no candidate inside the in-tile halo.
 __device__ __forceinline__ void push_straggler(const VerifyArgs& A, const SegJob& J, uint32_t s, uint32_t iseg,
@@ -433,33 +437,13 @@ __device__ __forceinline__ void push_straggler(const VerifyArgs& A, const SegJob
     if (idx < A.list_cap) A.list[idx] = StragEntry{s, iseg, (uint32_t)JH, flags};
 }
 
-// Hard evens of a fast block (no candidate p <= 129): the fast path counted
-// each as the placeholder p = P_HARD.  found_hard replaces it by the true p
-// (>= 131) or removes it and hands the even to K4.  Queue order is not even
-// order, hence the tie-aware max.
-template <bool PMIN>
-__device__ __forceinline__ void found_hard(uint32_t p, uint32_t il, uint32_t i0, uint32_t s, const SegJob& J,
-                                           const VerifyArgs& A, uint32_t jlim_small, K3Acc& acc) {
-    const uint32_t iseg = i0 + il;
-    if (p) {
-        acc.sp += p - P_HARD;
-        acc.spi += (uint64_t)(p - P_HARD) * il;
-        acc.observe(p, il);
-    } else {
-        acc.sp -= P_HARD;
-        acc.spi -= (uint64_t)P_HARD * il;
-        push_straggler(A, J, s, iseg, jlim_small, 0);
-    }
-    if constexpr (PMIN) A.pmin_out[iseg] = p;
-}
-
-// Level 2: windows k = 2 .. NWIN-1 of one even (one exit, p computed once).
+// Deep even of a fast block: windows k = ZBS/64 .. NWIN-1 (one exit).
 template <bool PMIN>
 __device__ __forceinline__ void deep_even(const uint32_t* tile, const uint64_t* pmr, uint32_t il, uint32_t i0,
                                           uint32_t s, const SegJob& J, const VerifyArgs& A, uint32_t jlim_small,
                                           K3Acc& acc) {
     const uint32_t x0 = (uint32_t)JH + il + 1;
-    uint32_t k = 2;
+    uint32_t k = ZBS / 64;
     uint64_t m = 0;
 #pragma unroll 1
     for (; k < (uint32_t)NWIN; ++k) {
@@ -467,7 +451,14 @@ __device__ __forceinline__ void deep_even(const uint32_t* tile, const uint64_t* 
         if (m) break;
     }
     const uint32_t p = m ? 3 + 2 * (64 * k + __clzll(m)) : 0;
-    found_hard<PMIN>(p, il, i0, s, J, A, jlim_small, acc);
+    if (p) {
+        acc.sp += p;
+        acc.spi += (uint64_t)p * il;
+        acc.observe(p, il);
+    } else {
+        push_straggler(A, J, s, i0 + il, jlim_small, 0);
+    }
+    if constexpr (PMIN) A.pmin_out[i0 + il] = p;
 }
 
 // Generic per-even check (low window, n = 4, q >= 3 limits, small p_small,
@@ -510,19 +501,20 @@ __device__ __forceinline__ void generic_even(const uint32_t* tile, const uint64_
     if constexpr (PMIN) A.pmin_out[iseg] = p;
 }
 
-// z of the 64-candidate window 0 of one even: index of the smallest
-// candidate p = 3 + 2z with n - p prime, 64 if none (w0..w2 hold the cells
-// [lo - sh, lo - sh + 96), the window starts at cell lo - sh + sh_t).
-__device__ __forceinline__ uint32_t zwin0(uint32_t w0, uint32_t w1, uint32_t w2, uint32_t sh_t, uint32_t pm_lo,
-                                          uint32_t pm_hi) {
-    const uint32_t l = __funnelshift_rc(w0, w1, sh_t) & pm_lo;
-    const uint32_t h = __funnelshift_rc(w1, w2, sh_t) & pm_hi;
-    return h ? __clz(h) : 32 + __clz(l);
+// sum of the bit indices set in x
+__device__ __forceinline__ uint32_t idx_sum(uint32_t x) {
+    return __popc(x & 0xAAAAAAAAu) + 2 * __popc(x & 0xCCCCCCCCu) + 4 * __popc(x & 0xF0F0F0F0u) +
+           8 * __popc(x & 0xFF00FF00u) + 16 * __popc(x & 0xFFFF0000u);
 }
 
-constexpr uint32_t CHUNK = 128;            // evens per warp iteration (4 per lane)
-constexpr uint32_t HQ = 64;                // per-warp level-2 queue
-constexpr uint32_t FLUSH_IT = 4;           // fast iterations between hard-even flushes
+// Bit-sliced scan of word w of a fast block: U = evens (bits) with no
+// candidate z < ZBS, F = ~U found, Z = planes of their z.
+__device__ __forceinline__ uint32_t scan_word(const uint32_t* tile, uint32_t w, uint32_t (&Z)[NPL]) {
+    const uint32_t* tp = tile + JH / 32 + w; // word B of the lane's top cells
+    uint32_t U = ~0u;
+    bs_scan128(tp[-4], tp[-3], tp[-2], tp[-1], tp[0], U, Z);
+    return U;
+}
 
 template <bool PMIN>
 __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
@@ -533,8 +525,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
     __shared__ uint32_t s_blk;
     __shared__ unsigned long long s_red[NWARPS][3];
     __shared__ unsigned long long s_key;
-    __shared__ uint16_t s_q1[NWARPS][FLUSH_IT * CHUNK]; // level-1 hard-even queue (offsets from base0)
-    __shared__ uint32_t s_q2[NWARPS][HQ];        // level-2 queue (evens needing windows k >= 2)
+    __shared__ uint32_t s_q[NWARPS][QCAP];       // deep-even queue (block even indices)
 
     for (uint32_t i = threadIdx.x; i < PAT_WORDS; i += blockDim.x) pat[i] = A.gpat[i];
     for (uint32_t i = threadIdx.x; i < (uint32_t)NWIN; i += blockDim.x) pmr[i] = A.pmr[i];
@@ -580,49 +571,39 @@ __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
         // p_small >= 8193), no n = 4, no injected even
         const bool fast = !low && jlim_small >= (uint32_t)JH - 1 && !inject_here;
         K3Acc acc;
-        uint32_t nfull = 0;       // evens [0, nfull) went through the fast path
+        const uint32_t nw = fast ? ne >> 5 : 0; // full words of the fast path
         if (fast) {
-            const uint32_t pm_lo = (uint32_t)pmr[0], pm_hi = (uint32_t)(pmr[0] >> 32);
-            const uint64_t pm1 = pmr[1];
-            uint16_t* q1 = s_q1[warp];
-            uint32_t* q2 = s_q2[warp];
-            uint32_t q2n = 0;     // warp-uniform level-2 length (< 32 between batches)
-            nfull = ne & ~(CHUNK - 1);
-            uint32_t zs = 0, tz = 0, iters = 0;
-            uint64_t hp = 0;
-            uint32_t base = warp * CHUNK;
-            while (base < nfull) {
-                // up to FLUSH_IT iterations; hard evens collected as bits 4k + t
-                uint32_t hm = 0;
-                const uint32_t base0 = base;
-#pragma unroll 1
-                for (uint32_t k = 0; k < FLUSH_IT && base < nfull; ++k, base += CHUNK * NWARPS) {
-                    // lane owns evens il0..il0+3: their 64-cell windows
-                    // [JH+il0+t-63, JH+il0+t] lie in 3 words (sh <= 29)
-                    const uint32_t il0 = base + 4 * lane;
-                    const uint32_t lo = il0 + (JH - 63);
-                    const uint32_t wi = lo >> 5, sh = lo & 31;
-                    const uint32_t w0 = tile[wi], w1 = tile[wi + 1], w2 = tile[wi + 2];
-                    const uint32_t z0 = zwin0(w0, w1, w2, sh, pm_lo, pm_hi);
-                    const uint32_t z1 = zwin0(w0, w1, w2, sh + 1, pm_lo, pm_hi);
-                    const uint32_t z2 = zwin0(w0, w1, w2, sh + 2, pm_lo, pm_hi);
-                    const uint32_t z3 = zwin0(w0, w1, w2, sh + 3, pm_lo, pm_hi);
-                    const uint32_t zsum = z0 + z1 + z2 + z3;
-                    zs += zsum;
-                    tz += z1 + 2 * z2 + 3 * z3;
-                    hp += (uint64_t)(12 + 2 * zsum) * il0;
-                    hm |= ((z0 >> 6) | ((z1 >> 5) & 2u) | ((z2 >> 4) & 4u) | ((z3 >> 3) & 8u)) << (4 * k);
-                    ++iters;
+            uint32_t* q = s_q[warp];
+            uint32_t qn = 0;  // warp-uniform queue length (< 32 between words)
+            uint32_t sp32 = 0; // sum p of the bit-sliced evens (< 2^32 per lane)
+            for (uint32_t wb = warp * 32; wb < nw; wb += THREADS) {
+                const uint32_t w = wb + lane;
+                uint32_t U = 0;
+                if (w < nw) {
+                    uint32_t Z[NPL];
+                    U = scan_word(tile, w, Z);
+                    const uint32_t F = ~U;
+                    // p = 3 + 2z: sum p and sum p * (bit index) of the word
+                    uint32_t P = 3 * __popc(F), Q = 3 * idx_sum(F);
+#pragma unroll
+                    for (int bp = 0; bp < NPL; ++bp) {
+                        P += (2u << bp) * __popc(Z[bp]);
+                        Q += (2u << bp) * idx_sum(Z[bp]);
+                    }
+                    sp32 += P;
+                    acc.spi += (uint64_t)Q + (uint64_t)(32 * w) * P;
                     if constexpr (PMIN) {
-                        A.pmin_out[i0 + il0 + 0] = z0 < 64 ? 3 + 2 * z0 : 0;
-                        A.pmin_out[i0 + il0 + 1] = z1 < 64 ? 3 + 2 * z1 : 0;
-                        A.pmin_out[i0 + il0 + 2] = z2 < 64 ? 3 + 2 * z2 : 0;
-                        A.pmin_out[i0 + il0 + 3] = z3 < 64 ? 3 + 2 * z3 : 0;
+                        for (uint32_t i = 0; i < 32; ++i) {
+                            if (!((F >> i) & 1)) continue;
+                            uint32_t z = 0;
+#pragma unroll
+                            for (int bp = 0; bp < NPL; ++bp) z |= ((Z[bp] >> i) & 1) << bp;
+                            A.pmin_out[i0 + 32 * w + i] = 3 + 2 * z;
+                        }
                     }
                 }
-                // compact this lane's hard bits into the warp's level-1 queue
-                // (u16 offsets from base0) with one warp prefix sum
-                const uint32_t c = __popc(hm);
+                // deep evens: compact into the warp queue, drain 32 at a time
+                const uint32_t c = __popc(U);
                 uint32_t incl = c;
 #pragma unroll
                 for (int o = 1; o < 32; o <<= 1) {
@@ -630,44 +611,37 @@ __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
                     if (lane >= (uint32_t)o) incl += y;
                 }
                 const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-                uint32_t pos = incl - c;
-                while (hm) {
-                    const uint32_t bit = __ffs(hm) - 1;
-                    hm &= hm - 1;
-                    q1[pos++] = (uint16_t)((bit >> 2) * (CHUNK * NWARPS) + 4 * lane + (bit & 3));
-                }
-                __syncwarp();
-                // level 1: window k = 1 for 32 hard evens at a time; misses go
-                // to the level-2 queue, drained 32 at a time
-                for (uint32_t e0 = 0; e0 < total; e0 += 32) {
-                    const uint32_t e = e0 + lane;
-                    const bool act = e < total;
-                    const uint32_t il = base0 + (act ? (uint32_t)q1[e] : 0u);
-                    const uint64_t m = act ? window_bits_hi(tile, (uint32_t)JH + il + 1 - 64) & pm1 : 0;
-                    if (m) found_hard<PMIN>(3 + 2 * (64 + __clzll(m)), il, i0, s, J, A, jlim_small, acc);
-                    const bool miss = act && !m;
-                    const uint32_t bal = __ballot_sync(0xffffffffu, miss);
-                    if (miss) q2[q2n + __popc(bal & ((1u << lane) - 1))] = il;
-                    q2n += __popc(bal);
+                if (qn + total <= QCAP) {
+                    uint32_t pos = qn + incl - c;
+                    while (U) {
+                        const uint32_t bit = __ffs(U) - 1;
+                        U &= U - 1;
+                        q[pos++] = 32 * w + bit;
+                    }
+                    qn += total;
                     __syncwarp();
-                    if (q2n >= 32) {
-                        deep_even<PMIN>(tile, pmr, q2[q2n - 32 + lane], i0, s, J, A, jlim_small, acc);
-                        q2n -= 32;
+                    while (qn >= 32) {
+                        deep_even<PMIN>(tile, pmr, q[qn - 32 + lane], i0, s, J, A, jlim_small, acc);
+                        qn -= 32;
+                        __syncwarp();
+                    }
+                } else {
+                    while (U) { // queue full: this lane's deep evens in place
+                        const uint32_t bit = __ffs(U) - 1;
+                        U &= U - 1;
+                        deep_even<PMIN>(tile, pmr, 32 * w + bit, i0, s, J, A, jlim_small, acc);
                     }
                     __syncwarp();
                 }
             }
-            if (lane < q2n) deep_even<PMIN>(tile, pmr, q2[lane], i0, s, J, A, jlim_small, acc);
+            if (lane < qn) deep_even<PMIN>(tile, pmr, q[lane], i0, s, J, A, jlim_small, acc);
             __syncwarp();
-            // p_t = 3 + 2 z_t: sum p = 12 per iteration + 2 sum z; sum p*il =
-            // sum P4*il0 + sum (p1 + 2 p2 + 3 p3) = hp + 18 iters + 2 tz
-            acc.sp += 12ull * iters + 2ull * zs;
-            acc.spi += hp + 18ull * iters + 2ull * tz;
+            acc.sp += sp32;
         }
         {
             // generic path (whole block, or the tail of a fast block)
             const uint32_t t0 = low ? (uint32_t)((J.a - 4) >> 1) : (uint32_t)JH;
-            for (uint32_t il = nfull + threadIdx.x; il < ne; il += blockDim.x)
+            for (uint32_t il = 32 * nw + threadIdx.x; il < ne; il += blockDim.x)
                 generic_even<PMIN>(tile, pmr, il, t0, i0, s, J, A, jlim_small, acc);
         }
         // ---- block reduction -> slot accumulators; key = p << 32 | ~iseg
@@ -698,23 +672,29 @@ __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
         }
         __syncthreads();
         uint64_t K = s_key;
-        if (nfull && K < ((uint64_t)P_HARD << 32)) {
-            // no in-tile p >= 131: the block max may be a fast even, whose
-            // index the fast path did not keep -- rescan window 0 exactly
-            const uint32_t pm_lo = (uint32_t)pmr[0], pm_hi = (uint32_t)(pmr[0] >> 32);
+        if (nw && K < ((uint64_t)(3 + 2 * ZBS) << 32)) {
+            // no deep even beat the bit-sliced range: the block max may be a
+            // bit-sliced even -- rescan for max z (smallest il on ties)
             uint32_t bz = 0, bi = 0xFFFFFFFFu;
-            for (uint32_t base = warp * CHUNK; base < nfull; base += CHUNK * NWARPS) {
-                const uint32_t il0 = base + 4 * lane;
-                const uint32_t lo = il0 + (JH - 63);
-                const uint32_t wi = lo >> 5, sh = lo & 31;
-                const uint32_t w0 = tile[wi], w1 = tile[wi + 1], w2 = tile[wi + 2];
+            for (uint32_t wb = warp * 32; wb < nw; wb += THREADS) {
+                const uint32_t w = wb + lane;
+                if (w >= nw) continue;
+                uint32_t Z[NPL];
+                uint32_t cand = ~scan_word(tile, w, Z);
+                if (!cand) continue;
+                uint32_t mz = 0;
 #pragma unroll
-                for (uint32_t t = 0; t < 4; ++t) {
-                    const uint32_t z = zwin0(w0, w1, w2, sh + t, pm_lo, pm_hi);
-                    if (z < 64 && (bi == 0xFFFFFFFFu || z > bz)) {
-                        bz = z;
-                        bi = il0 + t;
+                for (int bp = NPL - 1; bp >= 0; --bp) {
+                    const uint32_t t = cand & Z[bp];
+                    if (t) {
+                        cand = t;
+                        mz |= 1u << bp;
                     }
+                }
+                const uint32_t il = 32 * w + __ffs(cand) - 1;
+                if (bi == 0xFFFFFFFFu || mz > bz) { // words ascend per lane: ties keep the smaller il
+                    bz = mz;
+                    bi = il;
                 }
             }
             uint64_t kf = bi != 0xFFFFFFFFu ? (((uint64_t)(3 + 2 * bz) << 32) | (0xFFFFFFFFu - (i0 + bi))) : 0;
