@@ -61,7 +61,7 @@ struct Piece {
 struct Batch {
     cudaStream_t st = nullptr;
     SegJob* d_jobs = nullptr;
-    uint32_t* d_c0 = nullptr;
+    uint4* d_pmc = nullptr;           // per slot {p, magic, c0} of the tile primes
     uint32_t* d_qg = nullptr;
     SlotAcc* d_acc = nullptr;
     StragEntry* d_list = nullptr;
@@ -97,7 +97,6 @@ struct gb_dev {
     uint64_t iL0 = 0, iL1 = 0;          // large primes
     uint32_t* d_pat = nullptr;
     uint64_t* d_pmr = nullptr;
-    uint2* d_pm = nullptr;              // {p, magic} of primes [iA1, iB1)
     uint64_t max_piece = 0;
     uint64_t qg_stride = 0; // words per slot
     Batch batches[NBATCH];
@@ -143,7 +142,7 @@ static int batch_alloc(gb_dev* d, Batch& b, bool with_qg) {
     if (!b.st) CU(d, cudaStreamCreateWithFlags(&b.st, cudaStreamNonBlocking));
     uint32_t np = d->iB1 - d->iA0;
     CU(d, dmalloc(d->device, &b.d_jobs, SLOTS * sizeof(SegJob)));
-    CU(d, dmalloc(d->device, &b.d_c0, (size_t)SLOTS * std::max<uint32_t>(np, 1) * 4));
+    CU(d, dmalloc(d->device, &b.d_pmc, (size_t)SLOTS * std::max<uint32_t>(np, 1) * sizeof(uint4)));
     if (with_qg && d->iL1 > d->iL0) CU(d, dmalloc(d->device, &b.d_qg, (size_t)SLOTS * d->qg_stride * 4));
     CU(d, dmalloc(d->device, &b.d_acc, SLOTS * sizeof(SlotAcc)));
     CU(d, dmalloc(d->device, &b.d_list, (size_t)LIST_CAP * sizeof(StragEntry)));
@@ -162,7 +161,7 @@ static int batch_alloc(gb_dev* d, Batch& b, bool with_qg) {
 
 static void batch_free(gb_dev* d, Batch& b) {
     dfree(d->device, b.d_jobs);
-    dfree(d->device, b.d_c0);
+    dfree(d->device, b.d_pmc);
     dfree(d->device, b.d_qg);
     dfree(d->device, b.d_acc);
     dfree(d->device, b.d_list);
@@ -221,7 +220,7 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     }
     const uint32_t np = d->iB1 - d->iA0;
     if (np) {
-        CU(d, launch_segment_offsets(b.d_jobs, n, d->d_primes, d->iA0, np, b.d_c0, st));
+        CU(d, launch_segment_offsets(b.d_jobs, n, d->d_primes, d->iA0, np, b.d_pmc, st));
         d->launches++;
     }
     VerifyArgs A{};
@@ -233,8 +232,7 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     A.iA1 = d->iA1;
     A.iB1 = d->iB1;
     A.np = np;
-    A.c0 = b.d_c0;
-    A.pm = d->d_pm;
+    A.pmc = b.d_pmc;
     A.qg = large ? b.d_qg : nullptr;
     A.qg_stride_words = d->qg_stride;
     A.gpat = d->d_pat;
@@ -491,11 +489,7 @@ static int build_tables(gb_dev* d) {
     d->iB1 = (uint32_t)(std::upper_bound(hp.begin(), hp.end(), P_TILE_MAX) - hp.begin());
     d->iL0 = d->iB1;
     d->iL1 = total;
-    const uint32_t nm = d->iB1 > d->iA1 ? d->iB1 - d->iA1 : 0;
-    CU(d, dmalloc(d->device, &d->d_pm, std::max<uint32_t>(nm, 1) * sizeof(uint2)));
-    CU(d, launch_prime_magic(d->d_primes + d->iA1, nm, d->d_pm, d->sync.st));
-    CU(d, cudaStreamSynchronize(d->sync.st));
-    d->launches++;
+    CU(d, cudaStreamSynchronize(d->sync.st)); // tables ready before any batch stream
     return GB_OK;
 }
 
@@ -587,7 +581,6 @@ int gb_close(gb_dev* d) {
     dfree(d->device, d->flush_buf);
     dfree(d->device, d->d_pat);
     dfree(d->device, d->d_pmr);
-    dfree(d->device, d->d_pm);
     delete d;
     return GB_OK;
 }

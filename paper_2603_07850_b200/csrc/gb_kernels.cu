@@ -296,17 +296,19 @@ __global__ void k_compact(const uint32_t* __restrict__ bits, uint64_t n_words, u
 }
 
 // ============================================================ segment setup
-// c0[s*np + i] = cell (relative to the slot's qbase) of the first odd
-// multiple of tile prime i (index iA0 + i) >= max(p^2, qbase); ~0 if >= 2^32.
+// pmc[s*np + i] = {p, floor(2^32/p), c0, 0} of tile prime i (index iA0 + i):
+// c0 = cell (relative to the slot's qbase) of the first odd multiple of p
+// >= max(p^2, qbase); ~0 if >= 2^32.  One 16-B load per prime per block.
 __global__ void k_segment_offsets(const SegJob* __restrict__ jobs, uint32_t nslots,
                                   const uint32_t* __restrict__ primes, uint32_t iA0, uint32_t np,
-                                  uint32_t* __restrict__ c0) {
+                                  uint4* __restrict__ pmc) {
     uint64_t total = (uint64_t)nslots * np;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
          t += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t s = (uint32_t)(t / np), i = (uint32_t)(t % np);
-        uint64_t c = first_cell_u64(jobs[s].qbase, primes[iA0 + i]);
-        c0[t] = c >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c;
+        const uint32_t p = primes[iA0 + i];
+        uint64_t c = first_cell_u64(jobs[s].qbase, p);
+        pmc[t] = make_uint4(p, (uint32_t)((1ull << 32) / p), c >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c, 0u);
     }
 }
 
@@ -331,53 +333,68 @@ __global__ void k_large_strike(const SegJob* __restrict__ jobs, uint32_t nslots,
 }
 
 // ============================================================ K2 + K3
-// Offsets for the verify path from the per-segment c0 table.
-struct SegOffset {
-    const uint32_t* c0;  // this slot's c0 row, biased so that c0[i] is prime i's entry
-    uint32_t B;          // block start cell relative to qbase
-    bool low;            // window starts at q = 1
-    __device__ __forceinline__ uint32_t low_off(uint32_t p) const {
-        uint64_t c = ((uint64_t)p * p - 1) >> 1;
-        return c < W ? (uint32_t)c : W;
+// Window cell of the first strike of {p, m, c0} in the block starting at
+// cell B (relative to qbase): c0 - B when c0 >= B (>= W: no strike), else
+// (-(B - c0)) mod p by the magic m = floor(2^32/p) (quotient estimate low
+// by at most one).  Branch-free.
+__device__ __forceinline__ uint32_t block_off(const uint4 v, uint32_t B) {
+    const uint32_t p = v.x, m = v.y, c = v.z;
+    const uint32_t x = B - c;
+    uint32_t r = x - __umulhi(x, m) * p;
+    r = r >= p ? r - p : r;
+    const uint32_t neg = r ? p - r : 0u;
+    return c >= B ? min(c - B, W) : neg;
+}
+
+// low window (q_w = 1): first strike at p^2
+__device__ __forceinline__ uint32_t low_off(uint32_t p) {
+    const uint64_t c = ((uint64_t)p * p - 1) >> 1;
+    return c < W ? (uint32_t)c : W;
+}
+
+// Warp-cooperative strikes of one prime from window cell o: lane L strikes
+// o + L p + k 32p.  32p cells are p words, so the lane's bit (and mask) is
+// fixed and only the word index advances.
+__device__ __forceinline__ void strike_warp(uint32_t* tile, uint32_t o, uint32_t p, uint32_t lane) {
+    const uint32_t c = o + lane * p;
+    if (c >= W) return;
+    const uint32_t mask = __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, c);
+    uint32_t wi = c >> 5;
+    const uint32_t p2 = 2 * p, p3 = 3 * p, p4 = 4 * p;
+    for (; wi + p3 < (uint32_t)TILE_WORDS; wi += p4) {
+        atomicAnd(&tile[wi], mask);
+        atomicAnd(&tile[wi + p], mask);
+        atomicAnd(&tile[wi + p2], mask);
+        atomicAnd(&tile[wi + p3], mask);
     }
-    // p < 1024: integer remainder (warp-uniform, ~170 primes per block)
-    __device__ __forceinline__ uint32_t small(uint32_t i, uint32_t p) const {
-        if (low) return low_off(p);
-        uint32_t c = __ldg(c0 + i);
-        if (c >= B) return min(c - B, W);
-        uint32_t r = (B - c) % p;
-        return r ? p - r : 0;
-    }
-    // p >= 1024: remainder by the prime's magic m = floor(2^32 / p):
-    // q = umulhi(x, m) is floor(x/p) or one less, so one correction
-    __device__ __forceinline__ uint32_t large_m(uint32_t i, uint32_t p, uint32_t m) const {
-        if (low) return low_off(p);
-        uint32_t c = __ldg(c0 + i);
-        if (c >= B) return min(c - B, W);
-        const uint32_t x = B - c;
-        uint32_t r = x - __umulhi(x, m) * p;
-        if (r >= p) r -= p;
-        return r ? p - r : 0;
-    }
-};
+    for (; wi < (uint32_t)TILE_WORDS; wi += p) atomicAnd(&tile[wi], mask);
+}
 
 // K2 strikes of one verify block: warp-cooperative below P_WARP_MAX, one
-// thread per prime above (primes + magics interleaved as uint2 {p, m}).
-__device__ __forceinline__ void strike_verify(uint32_t* tile, const uint32_t* __restrict__ primes,
-                                              const uint2* __restrict__ pm, uint32_t iA0, uint32_t iA1,
-                                              uint32_t iB1, const SegOffset& off) {
+// thread per prime above.  pmc: this slot's {p, m, c0} row (index i - iA0).
+__device__ __forceinline__ void strike_verify(uint32_t* tile, const uint4* __restrict__ pmc, uint32_t nA,
+                                              uint32_t nB, uint32_t B, bool low) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t nwarps = blockDim.x >> 5;
-    for (uint32_t i = iA0 + warp; i < iA1; i += nwarps) {
-        const uint32_t p = primes[i];
-        const uint32_t o = off.small(i, p);
-        if (o >= W) continue;
-        strike_run(tile, o + lane * p, 32 * p);
+    if (low) {
+        for (uint32_t i = warp; i < nA; i += NWARPS) {
+            const uint32_t p = __ldg(&pmc[i].x);
+            const uint32_t o = low_off(p);
+            if (o < W) strike_warp(tile, o, p, lane);
+        }
+        for (uint32_t i = nA + threadIdx.x; i < nB; i += THREADS) {
+            const uint32_t p = __ldg(&pmc[i].x);
+            strike_run(tile, low_off(p), p);
+        }
+        return;
     }
-    const uint2* pmb = pm - iA1;
-    for (uint32_t i = iA1 + threadIdx.x; i < iB1; i += blockDim.x) {
-        const uint2 e = __ldg(pmb + i);
-        strike_run(tile, off.large_m(i, e.x, e.y), e.x);
+    for (uint32_t i = warp; i < nA; i += NWARPS) {
+        const uint4 v = __ldg(pmc + i);
+        const uint32_t o = block_off(v, B);
+        if (o < W) strike_warp(tile, o, v.x, lane);
+    }
+    for (uint32_t i = nA + threadIdx.x; i < nB; i += THREADS) {
+        const uint4 v = __ldg(pmc + i);
+        strike_run(tile, block_off(v, B), v.x);
     }
 }
 
@@ -552,8 +569,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
         presieve_window(tile, pat, q_w);
         __syncthreads();
         presieve_fixup(tile, q_w);
-        const SegOffset off{A.c0 + ((int64_t)s * A.np - (int64_t)A.iA0), B, low};
-        strike_verify(tile, A.primes, A.pm, A.iA0, A.iA1, A.iB1, off);
+        strike_verify(tile, A.pmc + (size_t)s * A.np, A.iA1 - A.iA0, A.iB1 - A.iA0, B, low);
         __syncthreads();
         if (A.qg != nullptr && !low && J.qg_words) {
             const uint32_t* g = A.qg + s * A.qg_stride_words + B / 32;
@@ -852,14 +868,6 @@ __global__ void k_finalize(const SegJob* __restrict__ jobs, uint32_t nslots, con
     }
 }
 
-// magic[i] = floor(2^32 / p) for the thread-per-prime tile primes, as {p, m}
-__global__ void k_prime_magic(const uint32_t* __restrict__ primes, uint32_t n, uint2* __restrict__ pm) {
-    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
-        const uint32_t p = primes[i];
-        pm[i] = make_uint2(p, (uint32_t)((1ull << 32) / p));
-    }
-}
-
 // ============================================================ smem peak
 // Conflict-free 128-bit shared-memory loads from every resident warp: the
 // measured roofline denominator of the fused kernel (128 B/clk/SM nominal).
@@ -894,11 +902,6 @@ cudaError_t launch_smem_peak(uint32_t iters, uint32_t* sink, int grid, cudaStrea
     k_smem_peak<<<grid, THREADS, 65536, st>>>(iters, sink);
     return cudaGetLastError();
 }
-cudaError_t launch_prime_magic(const uint32_t* primes, uint32_t n, uint2* pm, cudaStream_t st) {
-    if (!n) return cudaSuccess;
-    k_prime_magic<<<(n + 255) / 256, 256, 0, st>>>(primes, n, pm);
-    return cudaGetLastError();
-}
 cudaError_t launch_init_tables(uint32_t* pat, uint64_t* pmr, uint64_t p_small, cudaStream_t st) {
     k_init_tables<<<64, 256, 0, st>>>(pat, pmr, p_small);
     return cudaGetLastError();
@@ -929,11 +932,11 @@ cudaError_t launch_compact(const uint32_t* bits, uint64_t n_words, uint32_t chun
     return cudaGetLastError();
 }
 cudaError_t launch_segment_offsets(const SegJob* jobs, uint32_t nslots, const uint32_t* primes,
-                                   uint32_t iA0, uint32_t np, uint32_t* c0, cudaStream_t st) {
+                                   uint32_t iA0, uint32_t np, uint4* pmc, cudaStream_t st) {
     uint64_t total = (uint64_t)nslots * np;
     if (!total) return cudaSuccess;
     unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
-    k_segment_offsets<<<grid, 256, 0, st>>>(jobs, nslots, primes, iA0, np, c0);
+    k_segment_offsets<<<grid, 256, 0, st>>>(jobs, nslots, primes, iA0, np, pmc);
     return cudaGetLastError();
 }
 cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, uint64_t iL0,

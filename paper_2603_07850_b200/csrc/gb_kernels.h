@@ -27,9 +27,8 @@ struct VerifyArgs {
     uint32_t total_blocks;
     const uint32_t* primes;
     uint32_t iA0, iA1, iB1;       // tile prime index ranges
-    uint32_t np;                  // c0 row length (iB1 - iA0)
-    const uint32_t* c0;           // nslots * np
-    const uint2* pm;              // {p, floor(2^32/p)} of primes [iA1, iB1)
+    uint32_t np;                  // pmc row length (iB1 - iA0)
+    const uint4* pmc;             // nslots * np {p, floor(2^32/p), c0, 0}
     const uint32_t* qg;           // large-prime bitmask (nullptr = none)
     uint64_t qg_stride_words;
     const uint32_t* gpat;
@@ -64,7 +63,7 @@ cudaError_t launch_scan(const uint32_t* counts, uint64_t n, uint64_t* offsets, u
 cudaError_t launch_compact(const uint32_t* bits, uint64_t n_words, uint32_t chunk, const uint64_t* offsets,
                            uint64_t lo, uint32_t* primes, uint64_t n_chunks, cudaStream_t st);
 cudaError_t launch_segment_offsets(const SegJob* jobs, uint32_t nslots, const uint32_t* primes,
-                                   uint32_t iA0, uint32_t np, uint32_t* c0, cudaStream_t st);
+                                   uint32_t iA0, uint32_t np, uint4* pmc, cudaStream_t st);
 cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, uint64_t iL0,
                                 uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, cudaStream_t st);
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st);
@@ -76,7 +75,6 @@ cudaError_t launch_finalize(const SegJob* jobs, uint32_t nslots, const SlotAcc* 
                             DevRecord* out, cudaStream_t st);
 cudaError_t launch_phase2_one(uint64_t n, uint64_t* out, cudaStream_t st);
 cudaError_t launch_is_prime_batch(const uint64_t* v, uint8_t* out, uint64_t n, cudaStream_t st);
-cudaError_t launch_prime_magic(const uint32_t* primes, uint32_t n, uint2* pm, cudaStream_t st);
 cudaError_t launch_smem_peak(uint32_t iters, uint32_t* sink, int grid, cudaStream_t st);
 int verify_occupancy(int* blocks_per_sm);
 
