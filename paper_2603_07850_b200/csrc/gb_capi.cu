@@ -29,7 +29,7 @@ namespace {
 constexpr int NBATCH = 3;                 // batches in flight per device
 constexpr uint32_t SLOTS = 8;             // pieces per batch
 constexpr uint32_t LIST_CAP = 1u << 20;   // straggler entries per batch
-constexpr uint64_t MAX_PIECE = 1ull << 31;
+constexpr uint64_t MAX_PIECE = MAX_SEG_EVENS; // cells of a piece stay < 2^31 - 1 (block_off)
 
 thread_local std::string t_err;
 
@@ -94,6 +94,7 @@ struct gb_dev {
     uint64_t sqrt_bound = 0, n_primes = 0;
     uint32_t* d_primes = nullptr;
     uint32_t iA0 = 0, iA1 = 0, iB1 = 0; // tile prime index ranges
+    uint32_t iW1 = 0;                   // first tile prime >= W
     uint64_t iL0 = 0, iL1 = 0;          // large primes
     uint32_t* d_pat = nullptr;
     uint64_t* d_pmr = nullptr;
@@ -231,6 +232,7 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     A.iA0 = d->iA0;
     A.iA1 = d->iA1;
     A.iB1 = d->iB1;
+    A.iW1 = d->iW1;
     A.np = np;
     A.pmc = b.d_pmc;
     A.qg = large ? b.d_qg : nullptr;
@@ -487,6 +489,7 @@ static int build_tables(gb_dev* d) {
     d->iA0 = (uint32_t)(std::lower_bound(hp.begin(), hp.end(), FIRST_STRIKE_P) - hp.begin());
     d->iA1 = (uint32_t)(std::lower_bound(hp.begin(), hp.end(), P_WARP_MAX) - hp.begin());
     d->iB1 = (uint32_t)(std::upper_bound(hp.begin(), hp.end(), P_TILE_MAX) - hp.begin());
+    d->iW1 = std::max(d->iA1, std::min(d->iB1, (uint32_t)(std::lower_bound(hp.begin(), hp.end(), W) - hp.begin())));
     d->iL0 = d->iB1;
     d->iL1 = total;
     CU(d, cudaStreamSynchronize(d->sync.st)); // tables ready before any batch stream
@@ -903,7 +906,7 @@ int gb_smem_peak(gb_dev* d, double* bytes_per_s) {
         CU(d, cudaEventSynchronize(e1));
         float ms = 0;
         CU(d, cudaEventElapsedTime(&ms, e0, e1));
-        const double bytes = (double)grid * THREADS * iters * 8 * 16;
+        const double bytes = (double)grid * SMEM_PEAK_THREADS * iters * 8 * 16;
         best = std::max(best, bytes / (ms * 1e-3));
     }
     d->launches += 4;

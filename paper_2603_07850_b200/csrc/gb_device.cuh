@@ -16,16 +16,22 @@ namespace gbk {
 // the straggler kernel (K4), which continues the same ascending scan.
 constexpr int JH = 4096;                // in-tile Phase 1 candidates j < JH
 constexpr int NWIN = JH / 64;           // 64-candidate windows
-constexpr int W_LOG2 = 19;
+#ifndef GB_W_LOG2
+#define GB_W_LOG2 19
+#endif
+constexpr int W_LOG2 = GB_W_LOG2;
 constexpr uint32_t W = 1u << W_LOG2;    // cells per block window
 constexpr uint32_t E = W - JH;          // evens per block
 constexpr int TILE_WORDS = W / 32;      // u32 words of the window
-constexpr int THREADS = 512;            // threads per CTA of the fused kernel
+// one 1024-thread CTA per SM with a 128 KiB tile (W = 2^20), or two
+// 512-thread CTAs with 64 KiB tiles (W = 2^19): 32 warps per SM either way
+constexpr int THREADS = W_LOG2 >= 20 ? 1024 : 512; // threads per CTA of the fused kernel
+constexpr int CTAS_PER_SM = W_LOG2 >= 20 ? 1 : 2;
 constexpr int NWARPS = THREADS / 32;
 constexpr uint32_t P_TILE_MAX = 1u << 22; // base primes above: K_large (global strikes)
 constexpr uint32_t P_WARP_MAX = 1024;     // primes below: warp-cooperative strikes
 constexpr uint32_t FIRST_STRIKE_P = 53;   // primes below are in the presieve patterns
-constexpr uint32_t MAX_SEG_EVENS = 1u << 31; // device sub-segment limit
+constexpr uint32_t MAX_SEG_EVENS = 1u << 30; // device sub-segment (piece) limit
 
 // presieve pattern groups (products of small odd primes); pattern bit k is 0
 // iff 2k+1 is divisible by a prime of the group.  Stored with 64 bits of

@@ -296,9 +296,10 @@ __global__ void k_compact(const uint32_t* __restrict__ bits, uint64_t n_words, u
 }
 
 // ============================================================ segment setup
-// pmc[s*np + i] = {p, floor(2^32/p), c0, 0} of tile prime i (index iA0 + i):
-// c0 = cell (relative to the slot's qbase) of the first odd multiple of p
-// >= max(p^2, qbase); ~0 if >= 2^32.  One 16-B load per prime per block.
+// pmc[s*np + i] = {p, floor(2^32/p), p - 1 - c0, c0} of tile prime i (index
+// iA0 + i): c0 = cell (relative to the slot's qbase) of the first odd
+// multiple of p >= max(p^2, qbase), clamped to 2^31 - 1 (pieces hold fewer
+// cells, so a clamped c0 strikes nothing).  One 16-B load per prime per block.
 __global__ void k_segment_offsets(const SegJob* __restrict__ jobs, uint32_t nslots,
                                   const uint32_t* __restrict__ primes, uint32_t iA0, uint32_t np,
                                   uint4* __restrict__ pmc) {
@@ -307,8 +308,9 @@ __global__ void k_segment_offsets(const SegJob* __restrict__ jobs, uint32_t nslo
          t += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t s = (uint32_t)(t / np), i = (uint32_t)(t % np);
         const uint32_t p = primes[iA0 + i];
-        uint64_t c = first_cell_u64(jobs[s].qbase, p);
-        pmc[t] = make_uint4(p, (uint32_t)((1ull << 32) / p), c >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)c, 0u);
+        const uint64_t c = first_cell_u64(jobs[s].qbase, p);
+        const uint32_t c0 = c >= 0x7FFFFFFFull ? 0x7FFFFFFFu : (uint32_t)c;
+        pmc[t] = make_uint4(p, (uint32_t)((1ull << 32) / p), p - 1 - c0, c0);
     }
 }
 
@@ -333,17 +335,20 @@ __global__ void k_large_strike(const SegJob* __restrict__ jobs, uint32_t nslots,
 }
 
 // ============================================================ K2 + K3
-// Window cell of the first strike of {p, m, c0} in the block starting at
-// cell B (relative to qbase): c0 - B when c0 >= B (>= W: no strike), else
-// (-(B - c0)) mod p by the magic m = floor(2^32/p) (quotient estimate low
-// by at most one).  Branch-free.
+// Window cell of the first strike of {p, m, d = p - 1 - c0, c0} in the block
+// starting at cell B (relative to qbase); >= W means no strike.
+//   c0 >= B: c0 - B.   c0 < B: (c0 - B) mod p = p - 1 - ((B + d) mod p).
+// The mod is exact through the magic m = floor(2^32/p) (quotient low by at
+// most one).  When c0 - B >= p, B + d wraps and the mod term is some value
+// < p <= c0 - B, so a signed max selects the right case without a branch.
 __device__ __forceinline__ uint32_t block_off(const uint4 v, uint32_t B) {
-    const uint32_t p = v.x, m = v.y, c = v.z;
-    const uint32_t x = B - c;
-    uint32_t r = x - __umulhi(x, m) * p;
-    r = r >= p ? r - p : r;
-    const uint32_t neg = r ? p - r : 0u;
-    return c >= B ? min(c - B, W) : neg;
+    const uint32_t p = v.x;
+    const uint32_t y = B + v.z;
+    uint32_t r = y - __umulhi(y, v.y) * p;
+    r = min(r, r - p);
+    const int32_t o_mod = (int32_t)(p - 1 - r);
+    const int32_t o_dir = (int32_t)(v.w - B);
+    return (uint32_t)max(o_dir, o_mod);
 }
 
 // low window (q_w = 1): first strike at p^2
@@ -371,9 +376,10 @@ __device__ __forceinline__ void strike_warp(uint32_t* tile, uint32_t o, uint32_t
 }
 
 // K2 strikes of one verify block: warp-cooperative below P_WARP_MAX, one
-// thread per prime above.  pmc: this slot's {p, m, c0} row (index i - iA0).
+// thread per prime above; primes >= W (index >= nW) strike at most once.
+// pmc: this slot's {p, m, d, c0} row (index i - iA0).
 __device__ __forceinline__ void strike_verify(uint32_t* tile, const uint4* __restrict__ pmc, uint32_t nA,
-                                              uint32_t nB, uint32_t B, bool low) {
+                                              uint32_t nW, uint32_t nB, uint32_t B, bool low) {
     const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     if (low) {
         for (uint32_t i = warp; i < nA; i += NWARPS) {
@@ -392,9 +398,17 @@ __device__ __forceinline__ void strike_verify(uint32_t* tile, const uint4* __res
         const uint32_t o = block_off(v, B);
         if (o < W) strike_warp(tile, o, v.x, lane);
     }
-    for (uint32_t i = nA + threadIdx.x; i < nB; i += THREADS) {
+    for (uint32_t i = nA + threadIdx.x; i < nW; i += THREADS) {
         const uint4 v = __ldg(pmc + i);
         strike_run(tile, block_off(v, B), v.x);
+    }
+    const uint4* q = pmc + nW + threadIdx.x;
+    const uint4* const qe = pmc + nB;
+#pragma unroll 2
+    for (; q < qe; q += THREADS) {
+        const uint4 v = __ldg(q);
+        const uint32_t o = block_off(v, B);
+        if (o < W) strike(tile, o);
     }
 }
 
@@ -534,7 +548,7 @@ __device__ __forceinline__ uint32_t scan_word(const uint32_t* tile, uint32_t w, 
 }
 
 template <bool PMIN>
-__global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
+__global__ void __launch_bounds__(THREADS, CTAS_PER_SM) k_verify_blocks(VerifyArgs A) {
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t* tile = smem;                                  // TILE_WORDS + pad
     uint32_t* pat = smem + VERIFY_PAT_OFF;                  // PAT_WORDS
@@ -569,7 +583,7 @@ __global__ void __launch_bounds__(THREADS, 2) k_verify_blocks(VerifyArgs A) {
         presieve_window(tile, pat, q_w);
         __syncthreads();
         presieve_fixup(tile, q_w);
-        strike_verify(tile, A.pmc + (size_t)s * A.np, A.iA1 - A.iA0, A.iB1 - A.iA0, B, low);
+        strike_verify(tile, A.pmc + (size_t)s * A.np, A.iA1 - A.iA0, A.iW1 - A.iA0, A.iB1 - A.iA0, B, low);
         __syncthreads();
         if (A.qg != nullptr && !low && J.qg_words) {
             const uint32_t* g = A.qg + s * A.qg_stride_words + B / 32;
@@ -871,7 +885,7 @@ __global__ void k_finalize(const SegJob* __restrict__ jobs, uint32_t nslots, con
 // ============================================================ smem peak
 // Conflict-free 128-bit shared-memory loads from every resident warp: the
 // measured roofline denominator of the fused kernel (128 B/clk/SM nominal).
-__global__ void __launch_bounds__(THREADS, 2) k_smem_peak(uint32_t iters, uint32_t* sink) {
+__global__ void __launch_bounds__(SMEM_PEAK_THREADS, 2) k_smem_peak(uint32_t iters, uint32_t* sink) {
     extern __shared__ __align__(16) uint4 sbuf[]; // 64 KiB
     constexpr uint32_t N = 4096;
     for (uint32_t i = threadIdx.x; i < N; i += blockDim.x) sbuf[i] = make_uint4(i, i * 3, i * 5, i * 7);
@@ -899,7 +913,7 @@ cudaError_t launch_smem_peak(uint32_t iters, uint32_t* sink, int grid, cudaStrea
         cudaFuncSetAttribute(k_smem_peak, cudaFuncAttributeMaxDynamicSharedMemorySize, 65536);
         attr = true;
     }
-    k_smem_peak<<<grid, THREADS, 65536, st>>>(iters, sink);
+    k_smem_peak<<<grid, SMEM_PEAK_THREADS, 65536, st>>>(iters, sink);
     return cudaGetLastError();
 }
 cudaError_t launch_init_tables(uint32_t* pat, uint64_t* pmr, uint64_t p_small, cudaStream_t st) {

@@ -27,8 +27,9 @@ struct VerifyArgs {
     uint32_t total_blocks;
     const uint32_t* primes;
     uint32_t iA0, iA1, iB1;       // tile prime index ranges
+    uint32_t iW1;                 // first tile prime >= W (strikes a block at most once)
     uint32_t np;                  // pmc row length (iB1 - iA0)
-    const uint4* pmc;             // nslots * np {p, floor(2^32/p), c0, 0}
+    const uint4* pmc;             // nslots * np {p, floor(2^32/p), p - 1 - c0, c0}
     const uint32_t* qg;           // large-prime bitmask (nullptr = none)
     uint64_t qg_stride_words;
     const uint32_t* gpat;
@@ -77,5 +78,6 @@ cudaError_t launch_phase2_one(uint64_t n, uint64_t* out, cudaStream_t st);
 cudaError_t launch_is_prime_batch(const uint64_t* v, uint8_t* out, uint64_t n, cudaStream_t st);
 cudaError_t launch_smem_peak(uint32_t iters, uint32_t* sink, int grid, cudaStream_t st);
 int verify_occupancy(int* blocks_per_sm);
+constexpr int SMEM_PEAK_THREADS = 512; // k_smem_peak: 2 CTAs x 512 threads per SM
 
 } // namespace gbk
