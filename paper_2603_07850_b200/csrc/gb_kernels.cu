@@ -538,6 +538,28 @@ __device__ __forceinline__ uint32_t idx_sum(uint32_t x) {
            8 * __popc(x & 0xFF00FF00u) + 16 * __popc(x & 0xFFFF0000u);
 }
 
+// Deferred sum p * (bit index) of VACC words: V = bit-sliced per-position
+// sums of z (VPL planes), FC = per-position found counts (FPL planes);
+// p = 3 + 2z, so the sum is 2 sum_b 2^b idx(V_b) + 3 sum_k 2^k idx(FC_k).
+// Resets V and FC.
+constexpr uint32_t VACC = 4;
+constexpr int VPL = NPL + 2;   // 4 * 127 < 2^9
+constexpr int FPL = 3;         // 4 < 2^3
+__device__ __forceinline__ uint32_t vsum_by_index(uint32_t (&V)[VPL], uint32_t (&FC)[FPL]) {
+    uint32_t q = 0;
+#pragma unroll
+    for (int b = 0; b < VPL; ++b) {
+        q += (2u << b) * idx_sum(V[b]);
+        V[b] = 0;
+    }
+#pragma unroll
+    for (int k = 0; k < FPL; ++k) {
+        q += (3u << k) * idx_sum(FC[k]);
+        FC[k] = 0;
+    }
+    return q;
+}
+
 // Bit-sliced scan of word w of a fast block: U = evens (bits) with no
 // candidate z < ZBS, F = ~U found, Z = planes of their z.
 __device__ __forceinline__ uint32_t scan_word(const uint32_t* tile, uint32_t w, uint32_t (&Z)[NPL]) {
@@ -606,6 +628,15 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) k_verify_blocks(VerifyAr
             uint32_t* q = s_q[warp];
             uint32_t qn = 0;  // warp-uniform queue length (< 32 between words)
             uint32_t sp32 = 0; // sum p of the bit-sliced evens (< 2^32 per lane)
+            // sum p * (bit index) is deferred: z planes and found bits of up
+            // to VACC words are summed per bit position as bit-sliced
+            // counters V (z) and FC (found), then reduced by bit index once
+            uint32_t V[VPL], FC[FPL];
+#pragma unroll
+            for (int k = 0; k < VPL; ++k) V[k] = 0;
+#pragma unroll
+            for (int k = 0; k < FPL; ++k) FC[k] = 0;
+            uint32_t nacc = 0;
             for (uint32_t wb = warp * 32; wb < nw; wb += THREADS) {
                 const uint32_t w = wb + lane;
                 uint32_t U = 0;
@@ -613,15 +644,34 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) k_verify_blocks(VerifyAr
                     uint32_t Z[NPL];
                     U = scan_word(tile, w, Z);
                     const uint32_t F = ~U;
-                    // p = 3 + 2z: sum p and sum p * (bit index) of the word
-                    uint32_t P = 3 * __popc(F), Q = 3 * idx_sum(F);
+                    // p = 3 + 2z: sum p of the word (weight 32w below)
+                    uint32_t P = 3 * __popc(F);
 #pragma unroll
-                    for (int bp = 0; bp < NPL; ++bp) {
-                        P += (2u << bp) * __popc(Z[bp]);
-                        Q += (2u << bp) * idx_sum(Z[bp]);
-                    }
+                    for (int bp = 0; bp < NPL; ++bp) P += (2u << bp) * __popc(Z[bp]);
                     sp32 += P;
-                    acc.spi += (uint64_t)Q + (uint64_t)(32 * w) * P;
+                    acc.spi += (uint64_t)(32 * w) * P;
+                    // V += Z, FC += F (ripple-carry, bit-sliced)
+                    uint32_t cy = V[0] & Z[0];
+                    V[0] ^= Z[0];
+#pragma unroll
+                    for (int bp = 1; bp < NPL; ++bp) {
+                        const uint32_t v = V[bp], z = Z[bp];
+                        V[bp] = v ^ z ^ cy;
+                        cy = (v & z) | (cy & (v ^ z));
+                    }
+#pragma unroll
+                    for (int bp = NPL; bp < VPL; ++bp) {
+                        const uint32_t v = V[bp];
+                        V[bp] = v ^ cy;
+                        cy = v & cy;
+                    }
+                    cy = F;
+#pragma unroll
+                    for (int k = 0; k < FPL; ++k) {
+                        const uint32_t f = FC[k];
+                        FC[k] = f ^ cy;
+                        cy = f & cy;
+                    }
                     if constexpr (PMIN) {
                         for (uint32_t i = 0; i < 32; ++i) {
                             if (!((F >> i) & 1)) continue;
@@ -631,6 +681,10 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) k_verify_blocks(VerifyAr
                             A.pmin_out[i0 + 32 * w + i] = 3 + 2 * z;
                         }
                     }
+                }
+                if (++nacc == VACC) {
+                    acc.spi += vsum_by_index(V, FC);
+                    nacc = 0;
                 }
                 // deep evens: compact into the warp queue, drain 32 at a time
                 const uint32_t c = __popc(U);
@@ -666,6 +720,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) k_verify_blocks(VerifyAr
             }
             if (lane < qn) deep_even<PMIN>(tile, pmr, q[lane], i0, s, J, A, jlim_small, acc);
             __syncwarp();
+            if (nacc) acc.spi += vsum_by_index(V, FC);
             acc.sp += sp32;
         }
         {
