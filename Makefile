@@ -11,7 +11,7 @@ CSRC := $(PKG)/csrc
 BIN := $(PKG)/bin
 OBJ := build/obj
 CUDA_HOME ?= /usr/local/cuda
-NVFLAGS := -std=c++17 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -warn-spills -I$(CSRC) -Iinclude
+NVFLAGS := -std=c++17 -O3 $(ARCH) -lineinfo -Xcompiler -fPIC -Xptxas -warn-spills -I$(CSRC) -Iinclude $(NVEXTRA)
 CXXFLAGS := -std=c++20 -O2 -fPIC -Wall -Wextra -pthread -I$(CSRC)/include -Iinclude -I$(CUDA_HOME)/include
 LIB := $(PKG)/libgoldbach_b200.so
 

@@ -21,7 +21,8 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgoldbach_b200.so")
+# GB_LIB_PATH: load a differently built copy (tools/variants.sh timing runs)
+LIB_PATH = os.environ.get("GB_LIB_PATH") or os.path.join(HERE, "libgoldbach_b200.so")
 CLI_PATH = os.path.join(HERE, "bin", "goldbach")
 GB_REC_MAX_CE = 16
 

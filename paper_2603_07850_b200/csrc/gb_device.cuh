@@ -34,12 +34,13 @@ constexpr uint32_t FIRST_STRIKE_P = 53;   // primes below are in the presieve pa
 constexpr uint32_t MAX_SEG_EVENS = 1u << 30; // device sub-segment (piece) limit
 
 // presieve pattern groups (products of small odd primes); pattern bit k is 0
-// iff 2k+1 is divisible by a prime of the group.  Stored with 64 bits of
-// wrap-around so a 32-bit window at any phase is two word loads.
+// iff 2k+1 is divisible by a prime of the group.  Stored with wrap-around
+// words so four 32-bit windows at any phase are five word loads.
 __host__ __device__ constexpr uint32_t pg_p(int g) {
     return g == 0 ? 15015u : g == 1 ? 7429u : g == 2 ? 33263u : 82861u; // 3·5·7·11·13, 17·19·23, 29·31·37, 41·43·47
 }
-__host__ __device__ constexpr uint32_t pat_words(uint32_t P) { return (P + 64 + 31) / 32 + 1; }
+// words per pattern: a 5-word read (presieve_window) at any phase < P fits
+__host__ __device__ constexpr uint32_t pat_words(uint32_t P) { return (P + 31) / 32 + 5; }
 __host__ __device__ constexpr uint32_t pg_off(int g) {
     return (g > 0 ? pat_words(pg_p(0)) : 0u) + (g > 1 ? pat_words(pg_p(1)) : 0u) +
            (g > 2 ? pat_words(pg_p(2)) : 0u) + (g > 3 ? pat_words(pg_p(3)) : 0u);

@@ -88,29 +88,33 @@ struct SmemTables {
 };
 
 __device__ __forceinline__ void presieve_window(uint32_t* tile, const uint32_t* pat, uint64_t q_w) {
-    // phase of each group: k0 = ((q_w - 1)/2) mod P
+    // Each thread builds 4 consecutive tile words per step (one 16-B store):
+    // per pattern group 5 loads and 4 funnel shifts at one bit phase o,
+    // o = pattern bit of the first cell, advanced by 128 * blockDim mod P.
     uint32_t o[4], step[4];
     const uint64_t k0 = (q_w - 1) >> 1;
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
-        uint32_t P = pg_p(g);
-        uint32_t ph = (uint32_t)(k0 % P);
-        o[g] = (uint32_t)((ph + 32ull * threadIdx.x) % P);
-        step[g] = (32u * blockDim.x) % P;
+        const uint32_t P = pg_p(g);
+        const uint32_t ph = (uint32_t)(k0 % P);
+        o[g] = (uint32_t)((ph + 128ull * threadIdx.x) % P);
+        step[g] = (128u * blockDim.x) % P;
     }
-    for (uint32_t wd = threadIdx.x; wd < (uint32_t)TILE_WORDS; wd += blockDim.x) {
-        uint32_t v = ~0u;
+    for (uint32_t wd = 4 * threadIdx.x; wd < (uint32_t)TILE_WORDS; wd += 4 * blockDim.x) {
+        uint4 v = make_uint4(~0u, ~0u, ~0u, ~0u);
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
-            const uint32_t* pg = pat + pg_off(g);
-            uint32_t og = o[g];
-            uint32_t lo = pg[og >> 5], hi = pg[(og >> 5) + 1];
-            v &= __funnelshift_r(lo, hi, og & 31);
-            og += step[g];
-            if (og >= pg_p(g)) og -= pg_p(g);
-            o[g] = og;
+            const uint32_t* pg = pat + pg_off(g) + (o[g] >> 5);
+            const uint32_t sh = o[g]; // funnel shifts use sh mod 32
+            const uint32_t w0 = pg[0], w1 = pg[1], w2 = pg[2], w3 = pg[3], w4 = pg[4];
+            v.x &= __funnelshift_r(w0, w1, sh);
+            v.y &= __funnelshift_r(w1, w2, sh);
+            v.z &= __funnelshift_r(w2, w3, sh);
+            v.w &= __funnelshift_r(w3, w4, sh);
+            const uint32_t on = o[g] + step[g];
+            o[g] = min(on, on - pg_p(g)); // on < 2P
         }
-        tile[wd] = v;
+        *reinterpret_cast<uint4*>(tile + wd) = v;
     }
 }
 
@@ -398,13 +402,34 @@ __device__ __forceinline__ void strike_verify(uint32_t* tile, const uint4* __res
         const uint32_t o = block_off(v, B);
         if (o < W) strike_warp(tile, o, v.x, lane);
     }
-    for (uint32_t i = nA + threadIdx.x; i < nW; i += THREADS) {
-        const uint4 v = __ldg(pmc + i);
+    // thread per prime; the {p, m, d, c0} rows come from L2, so 4 (8) loads
+    // are issued before their strikes to keep several in flight per warp
+    const uint4* q = pmc + nA + threadIdx.x;
+    const uint4* qe = pmc + nW;
+    for (; q + 3 * THREADS < qe; q += 4 * THREADS) {
+        const uint4 v0 = __ldg(q), v1 = __ldg(q + THREADS), v2 = __ldg(q + 2 * THREADS),
+                    v3 = __ldg(q + 3 * THREADS);
+        strike_run(tile, block_off(v0, B), v0.x);
+        strike_run(tile, block_off(v1, B), v1.x);
+        strike_run(tile, block_off(v2, B), v2.x);
+        strike_run(tile, block_off(v3, B), v3.x);
+    }
+    for (; q < qe; q += THREADS) {
+        const uint4 v = __ldg(q);
         strike_run(tile, block_off(v, B), v.x);
     }
-    const uint4* q = pmc + nW + threadIdx.x;
-    const uint4* const qe = pmc + nB;
-#pragma unroll 2
+    q = pmc + nW + threadIdx.x;
+    qe = pmc + nB;
+    for (; q + 7 * THREADS < qe; q += 8 * THREADS) {
+        uint4 v[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(q + u * THREADS);
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+            const uint32_t o = block_off(v[u], B);
+            if (o < W) strike(tile, o);
+        }
+    }
     for (; q < qe; q += THREADS) {
         const uint4 v = __ldg(q);
         const uint32_t o = block_off(v, B);
@@ -454,6 +479,7 @@ struct K3Acc {
 // evens per lane (gb_bitslice.cuh); the few evens left ("deep") continue
 // per even from window ZBS/64.
 constexpr uint32_t ZBS = 128;
+static_assert(E < (1u << 24), "deep queue entries pack il in 24 bits");
 constexpr int NPL = BS_SCAN128_PLANES;   // z planes
 constexpr uint32_t QCAP = 160;           // per-warp deep-even queue
 
@@ -490,6 +516,40 @@ __device__ __forceinline__ void deep_even(const uint32_t* tile, const uint64_t* 
         push_straggler(A, J, s, i0 + il, jlim_small, 0);
     }
     if constexpr (PMIN) A.pmin_out[i0 + il] = p;
+}
+
+// One round over the warp's deep-even queue: the top n entries (il | k << 24)
+// each test ONE window k; misses are pushed back with k + 1, so no lane idles
+// while another walks many windows.  Returns the new queue length.
+template <bool PMIN>
+__device__ __forceinline__ uint32_t deep_round(const uint32_t* tile, const uint64_t* pmr, uint32_t* q, uint32_t qn,
+                                               uint32_t n, uint32_t lane, uint32_t i0, uint32_t s, const SegJob& J,
+                                               const VerifyArgs& A, uint32_t jlim_small, K3Acc& acc) {
+    qn -= n;
+    const bool act = lane < n;
+    const uint32_t e = act ? q[qn + lane] : 0u;
+    __syncwarp();
+    bool again = false;
+    if (act) {
+        const uint32_t il = e & 0xFFFFFFu, k = e >> 24;
+        const uint64_t m = window_bits_hi(tile, (uint32_t)JH + il + 1 - 64 * k) & pmr[k];
+        if (m) {
+            const uint32_t p = 3 + 2 * (64 * k + __clzll(m));
+            acc.sp += p;
+            acc.spi += (uint64_t)p * il;
+            acc.observe(p, il);
+            if constexpr (PMIN) A.pmin_out[i0 + il] = p;
+        } else if (k + 1 < (uint32_t)NWIN) {
+            again = true;
+        } else {
+            push_straggler(A, J, s, i0 + il, jlim_small, 0);
+            if constexpr (PMIN) A.pmin_out[i0 + il] = 0;
+        }
+    }
+    const uint32_t bal = __ballot_sync(0xffffffffu, again);
+    if (again) q[qn + __popc(bal & ((1u << lane) - 1))] = e + (1u << 24);
+    __syncwarp();
+    return qn + __popc(bal);
 }
 
 // Generic per-even check (low window, n = 4, q >= 3 limits, small p_small,
@@ -700,15 +760,11 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) k_verify_blocks(VerifyAr
                     while (U) {
                         const uint32_t bit = __ffs(U) - 1;
                         U &= U - 1;
-                        q[pos++] = 32 * w + bit;
+                        q[pos++] = (32 * w + bit) | ((ZBS / 64) << 24);
                     }
                     qn += total;
                     __syncwarp();
-                    while (qn >= 32) {
-                        deep_even<PMIN>(tile, pmr, q[qn - 32 + lane], i0, s, J, A, jlim_small, acc);
-                        qn -= 32;
-                        __syncwarp();
-                    }
+                    while (qn >= 32) qn = deep_round<PMIN>(tile, pmr, q, qn, 32, lane, i0, s, J, A, jlim_small, acc);
                 } else {
                     while (U) { // queue full: this lane's deep evens in place
                         const uint32_t bit = __ffs(U) - 1;
@@ -718,8 +774,7 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) k_verify_blocks(VerifyAr
                     __syncwarp();
                 }
             }
-            if (lane < qn) deep_even<PMIN>(tile, pmr, q[lane], i0, s, J, A, jlim_small, acc);
-            __syncwarp();
+            while (qn) qn = deep_round<PMIN>(tile, pmr, q, qn, min(qn, 32u), lane, i0, s, J, A, jlim_small, acc);
             if (nacc) acc.spi += vsum_by_index(V, FC);
             acc.sp += sp32;
         }
