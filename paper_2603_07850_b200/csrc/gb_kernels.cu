@@ -397,10 +397,21 @@ __device__ __forceinline__ void strike_verify(uint32_t* tile, const uint4* __res
         }
         return;
     }
-    for (uint32_t i = warp; i < nA; i += NWARPS) {
-        const uint4 v = __ldg(pmc + i);
-        const uint32_t o = block_off(v, B);
-        if (o < W) strike_warp(tile, o, v.x, lane);
+    {
+        // warp-cooperative primes warp, warp + NWARPS, ...: the lanes load
+        // the rows and compute the offsets in parallel, then stride in turn
+        const uint32_t nmine = warp < nA ? (nA - warp + NWARPS - 1) / NWARPS : 0; // <= 32
+        uint32_t pm = 0, om = W;
+        if (lane < nmine) {
+            const uint4 v = __ldg(pmc + warp + NWARPS * lane);
+            pm = v.x;
+            om = block_off(v, B);
+        }
+        for (uint32_t k = 0; k < nmine; ++k) {
+            const uint32_t o = __shfl_sync(0xffffffffu, om, k);
+            const uint32_t p = __shfl_sync(0xffffffffu, pm, k);
+            if (o < W) strike_warp(tile, o, p, lane);
+        }
     }
     // thread per prime; the {p, m, d, c0} rows come from L2, so 4 (8) loads
     // are issued before their strikes to keep several in flight per warp
@@ -479,6 +490,7 @@ struct K3Acc {
 // evens per lane (gb_bitslice.cuh); the few evens left ("deep") continue
 // per even from window ZBS/64.
 constexpr uint32_t ZBS = 128;
+static_assert(P_WARP_MAX / 2 <= 32 * NWARPS, "warp-cooperative primes: at most 32 per warp");
 static_assert(E < (1u << 24), "deep queue entries pack il in 24 bits");
 constexpr int NPL = BS_SCAN128_PLANES;   // z planes
 constexpr uint32_t QCAP = 160;           // per-warp deep-even queue
