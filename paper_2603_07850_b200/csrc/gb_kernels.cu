@@ -22,6 +22,10 @@
 #include <algorithm>
 #include <cstdio>
 
+#ifndef GB_WS
+#define GB_WS 1   // warp-specialised fused kernel (sieve and check warp groups, 2 tiles)
+#endif
+
 namespace gbk {
 
 // ============================================================ table init
@@ -87,7 +91,8 @@ struct SmemTables {
     uint32_t pat[PAT_WORDS];
 };
 
-__device__ __forceinline__ void presieve_window(uint32_t* tile, const uint32_t* pat, uint64_t q_w) {
+__device__ __forceinline__ void presieve_window(uint32_t* tile, const uint32_t* pat, uint64_t q_w, uint32_t tid,
+                                                uint32_t nthr) {
     // Each thread builds 4 consecutive tile words per step (one 16-B store):
     // per pattern group 5 loads and 4 funnel shifts at one bit phase o,
     // o = pattern bit of the first cell, advanced by 128 * blockDim mod P.
@@ -97,10 +102,10 @@ __device__ __forceinline__ void presieve_window(uint32_t* tile, const uint32_t* 
     for (int g = 0; g < 4; ++g) {
         const uint32_t P = pg_p(g);
         const uint32_t ph = (uint32_t)(k0 % P);
-        o[g] = (uint32_t)((ph + 128ull * threadIdx.x) % P);
-        step[g] = (128u * blockDim.x) % P;
+        o[g] = (uint32_t)((ph + 128ull * tid) % P);
+        step[g] = (128u * nthr) % P;
     }
-    for (uint32_t wd = 4 * threadIdx.x; wd < (uint32_t)TILE_WORDS; wd += 4 * blockDim.x) {
+    for (uint32_t wd = 4 * tid; wd < (uint32_t)TILE_WORDS; wd += 4 * nthr) {
         uint4 v = make_uint4(~0u, ~0u, ~0u, ~0u);
 #pragma unroll
         for (int g = 0; g < 4; ++g) {
@@ -119,8 +124,8 @@ __device__ __forceinline__ void presieve_window(uint32_t* tile, const uint32_t* 
 }
 
 // After presieve: restore the pattern primes themselves and clear q = 1.
-__device__ __forceinline__ void presieve_fixup(uint32_t* tile, uint64_t q_w) {
-    if (threadIdx.x == 0 && q_w <= 47) {
+__device__ __forceinline__ void presieve_fixup(uint32_t* tile, uint64_t q_w, uint32_t tid) {
+    if (tid == 0 && q_w <= 47) {
         if (q_w == 1) atomicAnd(&tile[0], ~1u);
 #pragma unroll
         for (int t = 0; t < 14; ++t) {
@@ -194,9 +199,9 @@ __global__ void __launch_bounds__(THREADS) k_sieve_interval(uint64_t lo, uint64_
     const uint64_t nblk = (n_cells + W - 1) / W;
     for (uint64_t blk = blockIdx.x; blk < nblk; blk += gridDim.x) {
         const uint64_t q_w = lo + 2 * blk * (uint64_t)W;
-        presieve_window(tile, pat, q_w);
+        presieve_window(tile, pat, q_w, threadIdx.x, blockDim.x);
         __syncthreads();
-        presieve_fixup(tile, q_w);
+        presieve_fixup(tile, q_w, threadIdx.x);
         strike_primes(tile, primes, iA0, iA1, iB1, DirectOffset{q_w});
         __syncthreads();
         const uint64_t base_word = blk * (W / 32);
@@ -379,19 +384,20 @@ __device__ __forceinline__ void strike_warp(uint32_t* tile, uint32_t o, uint32_t
     for (; wi < (uint32_t)TILE_WORDS; wi += p) atomicAnd(&tile[wi], mask);
 }
 
-// K2 strikes of one verify block: warp-cooperative below P_WARP_MAX, one
+// K2 strikes of one verify block by a group of THREADS threads (tid = the
+// thread's index in the group): warp-cooperative below P_WARP_MAX, one
 // thread per prime above; primes >= W (index >= nW) strike at most once.
 // pmc: this slot's {p, m, d, c0} row (index i - iA0).
 __device__ __forceinline__ void strike_verify(uint32_t* tile, const uint4* __restrict__ pmc, uint32_t nA,
-                                              uint32_t nW, uint32_t nB, uint32_t B, bool low) {
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+                                              uint32_t nW, uint32_t nB, uint32_t B, bool low, uint32_t tid) {
+    const uint32_t lane = tid & 31, warp = tid >> 5;
     if (low) {
         for (uint32_t i = warp; i < nA; i += NWARPS) {
             const uint32_t p = __ldg(&pmc[i].x);
             const uint32_t o = low_off(p);
             if (o < W) strike_warp(tile, o, p, lane);
         }
-        for (uint32_t i = nA + threadIdx.x; i < nB; i += THREADS) {
+        for (uint32_t i = nA + tid; i < nB; i += THREADS) {
             const uint32_t p = __ldg(&pmc[i].x);
             strike_run(tile, low_off(p), p);
         }
@@ -415,7 +421,7 @@ __device__ __forceinline__ void strike_verify(uint32_t* tile, const uint4* __res
     }
     // thread per prime; the {p, m, d, c0} rows come from L2, so 4 (8) loads
     // are issued before their strikes to keep several in flight per warp
-    const uint4* q = pmc + nA + threadIdx.x;
+    const uint4* q = pmc + nA + tid;
     const uint4* qe = pmc + nW;
     for (; q + 3 * THREADS < qe; q += 4 * THREADS) {
         const uint4 v0 = __ldg(q), v1 = __ldg(q + THREADS), v2 = __ldg(q + 2 * THREADS),
@@ -429,7 +435,7 @@ __device__ __forceinline__ void strike_verify(uint32_t* tile, const uint4* __res
         const uint4 v = __ldg(q);
         strike_run(tile, block_off(v, B), v.x);
     }
-    q = pmc + nW + threadIdx.x;
+    q = pmc + nW + tid;
     qe = pmc + nB;
     for (; q + 7 * THREADS < qe; q += 8 * THREADS) {
         uint4 v[8];
@@ -641,6 +647,239 @@ __device__ __forceinline__ uint32_t scan_word(const uint32_t* tile, uint32_t w, 
     return U;
 }
 
+// Barrier of one group of THREADS threads (id 0 = the whole 512-thread CTA).
+__device__ __forceinline__ void gbar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(THREADS) : "memory"); }
+__device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+__device__ __forceinline__ void nb_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
+
+// Where flat block fb of a batch lies: slot, block of the slot, window.
+struct BlockInfo {
+    SegJob J;
+    uint64_t q_w;   // q of the window's cell 0
+    uint32_t s, b;  // slot, block index within the slot
+    uint32_t B;     // window start cell relative to the slot's qbase
+    bool low;       // window at q = 1
+};
+
+__device__ __forceinline__ BlockInfo block_info(const VerifyArgs& A, uint32_t fb) {
+    BlockInfo I;
+    uint32_t s = 0; // few slots: linear scan
+    while (s + 1 < A.nslots && A.jobs[s + 1].block_prefix <= fb) ++s;
+    I.s = s;
+    I.J = A.jobs[s];
+    I.b = fb - I.J.block_prefix;
+    I.low = I.b < I.J.b1;
+    I.q_w = I.low ? 1ull : I.J.qbase + 2ull * (uint64_t)(I.b - I.J.b1) * E;
+    I.B = I.low ? 0u : (I.b - I.J.b1) * E;
+    return I;
+}
+
+// K2: sieve block I into tile by one group (tid = index in the group).  On
+// return this thread's strikes are issued; the caller's barrier publishes.
+__device__ __forceinline__ void sieve_block(const VerifyArgs& A, uint32_t* tile, const uint32_t* pat,
+                                            const BlockInfo& I, uint32_t tid, int bar) {
+    presieve_window(tile, pat, I.q_w, tid, THREADS);
+    gbar(bar);
+    presieve_fixup(tile, I.q_w, tid);
+    strike_verify(tile, A.pmc + (size_t)I.s * A.np, A.iA1 - A.iA0, A.iW1 - A.iA0, A.iB1 - A.iA0, I.B, I.low,
+                  tid);
+    if (A.qg != nullptr && !I.low && I.J.qg_words) {
+        gbar(bar);
+        const uint32_t* g = A.qg + I.s * A.qg_stride_words + I.B / 32;
+        const uint32_t lim = min((uint32_t)TILE_WORDS, I.J.qg_words - I.B / 32);
+        for (uint32_t wd = tid; wd < lim; wd += THREADS) tile[wd] &= __ldg(g + wd);
+    }
+}
+
+// K3: minimal p of every even of block I over the sieved tile, by one group;
+// the block's sums / max key go to the slot accumulators.
+template <bool PMIN>
+__device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t* tile, const uint64_t* pmr,
+                                            const BlockInfo& I, uint32_t tid, int bar,
+                                            unsigned long long (*s_red)[3], unsigned long long* s_key_p,
+                                            uint32_t (*s_q)[QCAP]) {
+    const uint32_t lane = tid & 31, warp = tid >> 5;
+    const uint32_t jlim_small = A.p_small >= 3 ? (uint32_t)min((A.p_small - 3) / 2, (uint64_t)0xFFFFFFFFu) : 0;
+    const uint32_t s = I.s, b = I.b;
+    const SegJob& J = I.J;
+    const bool low = I.low;
+    unsigned long long& s_key = *s_key_p;
+    // ---- K3: minimal p per even, while the tile is in shared memory
+    const uint32_t i0 = b * E;
+    const uint32_t ne = min(E, J.evens - i0);
+    const uint64_t n_first = J.a + 2ull * i0, n_last = n_first + 2ull * (ne - 1);
+    const bool inject_here = (A.inject & 1) == 0 && A.inject >= n_first && A.inject <= n_last;
+    // fast blocks: every even has all NWIN windows valid (n >= 8196,
+    // p_small >= 8193), no n = 4, no injected even
+    const bool fast = !low && jlim_small >= (uint32_t)JH - 1 && !inject_here;
+    K3Acc acc;
+    const uint32_t nw = fast ? ne >> 5 : 0; // full words of the fast path
+    if (fast) {
+        uint32_t* q = s_q[warp];
+        uint32_t qn = 0;  // warp-uniform queue length (< 32 between words)
+        uint32_t sp32 = 0; // sum p of the bit-sliced evens (< 2^32 per lane)
+        // sum p * (bit index) is deferred: z planes and found bits of up
+        // to VACC words are summed per bit position as bit-sliced
+        // counters V (z) and FC (found), then reduced by bit index once
+        uint32_t V[VPL], FC[FPL];
+#pragma unroll
+        for (int k = 0; k < VPL; ++k) V[k] = 0;
+#pragma unroll
+        for (int k = 0; k < FPL; ++k) FC[k] = 0;
+        uint32_t nacc = 0;
+        for (uint32_t wb = warp * 32; wb < nw; wb += THREADS) {
+            const uint32_t w = wb + lane;
+            uint32_t U = 0;
+            if (w < nw) {
+                uint32_t Z[NPL];
+                U = scan_word(tile, w, Z);
+                const uint32_t F = ~U;
+                // p = 3 + 2z: sum p of the word (weight 32w below)
+                uint32_t P = 3 * __popc(F);
+#pragma unroll
+                for (int bp = 0; bp < NPL; ++bp) P += (2u << bp) * __popc(Z[bp]);
+                sp32 += P;
+                acc.spi += (uint64_t)(32 * w) * P;
+                // V += Z, FC += F (ripple-carry, bit-sliced)
+                uint32_t cy = V[0] & Z[0];
+                V[0] ^= Z[0];
+#pragma unroll
+                for (int bp = 1; bp < NPL; ++bp) {
+                    const uint32_t v = V[bp], z = Z[bp];
+                    V[bp] = v ^ z ^ cy;
+                    cy = (v & z) | (cy & (v ^ z));
+                }
+#pragma unroll
+                for (int bp = NPL; bp < VPL; ++bp) {
+                    const uint32_t v = V[bp];
+                    V[bp] = v ^ cy;
+                    cy = v & cy;
+                }
+                cy = F;
+#pragma unroll
+                for (int k = 0; k < FPL; ++k) {
+                    const uint32_t f = FC[k];
+                    FC[k] = f ^ cy;
+                    cy = f & cy;
+                }
+                if constexpr (PMIN) {
+                    for (uint32_t i = 0; i < 32; ++i) {
+                        if (!((F >> i) & 1)) continue;
+                        uint32_t z = 0;
+#pragma unroll
+                        for (int bp = 0; bp < NPL; ++bp) z |= ((Z[bp] >> i) & 1) << bp;
+                        A.pmin_out[i0 + 32 * w + i] = 3 + 2 * z;
+                    }
+                }
+            }
+            if (++nacc == VACC) {
+                acc.spi += vsum_by_index(V, FC);
+                nacc = 0;
+            }
+            // deep evens: compact into the warp queue, drain 32 at a time
+            const uint32_t c = __popc(U);
+            uint32_t incl = c;
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                if (lane >= (uint32_t)o) incl += y;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            if (qn + total <= QCAP) {
+                uint32_t pos = qn + incl - c;
+                while (U) {
+                    const uint32_t bit = __ffs(U) - 1;
+                    U &= U - 1;
+                    q[pos++] = (32 * w + bit) | ((ZBS / 64) << 24);
+                }
+                qn += total;
+                __syncwarp();
+                while (qn >= 32) qn = deep_round<PMIN>(tile, pmr, q, qn, 32, lane, i0, s, J, A, jlim_small, acc);
+            } else {
+                while (U) { // queue full: this lane's deep evens in place
+                    const uint32_t bit = __ffs(U) - 1;
+                    U &= U - 1;
+                    deep_even<PMIN>(tile, pmr, 32 * w + bit, i0, s, J, A, jlim_small, acc);
+                }
+                __syncwarp();
+            }
+        }
+        while (qn) qn = deep_round<PMIN>(tile, pmr, q, qn, min(qn, 32u), lane, i0, s, J, A, jlim_small, acc);
+        if (nacc) acc.spi += vsum_by_index(V, FC);
+        acc.sp += sp32;
+    }
+    {
+        // generic path (whole block, or the tail of a fast block)
+        const uint32_t t0 = low ? (uint32_t)((J.a - 4) >> 1) : (uint32_t)JH;
+        for (uint32_t il = 32 * nw + tid; il < ne; il += THREADS)
+            generic_even<PMIN>(tile, pmr, il, t0, i0, s, J, A, jlim_small, acc);
+    }
+    // ---- block reduction -> slot accumulators; key = p << 32 | ~iseg
+    uint64_t key = acc.mp ? (((uint64_t)acc.mp << 32) | (0xFFFFFFFFu - (i0 + acc.mi))) : 0;
+    uint64_t sp64 = acc.sp, spi = acc.spi + (uint64_t)i0 * acc.sp;
+    for (int o = 16; o; o >>= 1) {
+        sp64 += __shfl_xor_sync(0xffffffffu, sp64, o);
+        spi += __shfl_xor_sync(0xffffffffu, spi, o);
+        const uint64_t ok = __shfl_xor_sync(0xffffffffu, key, o);
+        key = ok > key ? ok : key;
+    }
+    if (lane == 0) {
+        s_red[warp][0] = sp64;
+        s_red[warp][1] = spi;
+        s_red[warp][2] = key;
+    }
+    gbar(bar);
+    if (tid == 0) {
+        uint64_t S = 0, SPI = 0, K = 0;
+        for (int w = 0; w < NWARPS; ++w) {
+            S += s_red[w][0];
+            SPI += s_red[w][1];
+            K = s_red[w][2] > K ? s_red[w][2] : K;
+        }
+        atomicAdd(&A.acc[s].sum, (unsigned long long)S);
+        atomicAdd(&A.acc[s].hash, (unsigned long long)((J.a >> 1) * S + SPI));
+        s_key = K;
+    }
+    gbar(bar);
+    uint64_t K = s_key;
+    if (nw && K < ((uint64_t)(3 + 2 * ZBS) << 32)) {
+        // no deep even beat the bit-sliced range: the block max may be a
+        // bit-sliced even -- rescan for max z (smallest il on ties)
+        uint32_t bz = 0, bi = 0xFFFFFFFFu;
+        for (uint32_t wb = warp * 32; wb < nw; wb += THREADS) {
+            const uint32_t w = wb + lane;
+            if (w >= nw) continue;
+            uint32_t Z[NPL];
+            uint32_t cand = ~scan_word(tile, w, Z);
+            if (!cand) continue;
+            uint32_t mz = 0;
+#pragma unroll
+            for (int bp = NPL - 1; bp >= 0; --bp) {
+                const uint32_t t = cand & Z[bp];
+                if (t) {
+                    cand = t;
+                    mz |= 1u << bp;
+                }
+            }
+            const uint32_t il = 32 * w + __ffs(cand) - 1;
+            if (bi == 0xFFFFFFFFu || mz > bz) { // words ascend per lane: ties keep the smaller il
+                bz = mz;
+                bi = il;
+            }
+        }
+        uint64_t kf = bi != 0xFFFFFFFFu ? (((uint64_t)(3 + 2 * bz) << 32) | (0xFFFFFFFFu - (i0 + bi))) : 0;
+        for (int o = 16; o; o >>= 1) {
+            const uint64_t ok = __shfl_xor_sync(0xffffffffu, kf, o);
+            kf = ok > kf ? ok : kf;
+        }
+        if (lane == 0) atomicMax(&s_key, (unsigned long long)kf);
+        gbar(bar);
+        K = s_key;
+    }
+    if (tid == 0 && K) atomicMax(&A.acc[s].key, (unsigned long long)K);
+}
+
+// Fused sieve + check, one 512-thread CTA per block at a time (2 per SM).
 template <bool PMIN>
 __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) k_verify_blocks(VerifyArgs A) {
     extern __shared__ __align__(16) uint32_t smem[];
@@ -655,210 +894,82 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) k_verify_blocks(VerifyAr
     for (uint32_t i = threadIdx.x; i < PAT_WORDS; i += blockDim.x) pat[i] = A.gpat[i];
     for (uint32_t i = threadIdx.x; i < (uint32_t)NWIN; i += blockDim.x) pmr[i] = A.pmr[i];
     for (uint32_t i = threadIdx.x; i < 4; i += blockDim.x) tile[TILE_WORDS + i] = 0;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const uint32_t jlim_small = A.p_small >= 3 ? (uint32_t)min((A.p_small - 3) / 2, (uint64_t)0xFFFFFFFFu) : 0;
-
+    // block claims: thread 0 requests the next block as soon as the current
+    // one starts, so the global atomic's round trip overlaps the sieve
+    uint32_t fb_next = 0;
+    if (threadIdx.x == 0) fb_next = atomicAdd(A.block_counter, 1u);
     for (;;) {
-        __syncthreads();
-        if (threadIdx.x == 0) s_blk = atomicAdd(A.block_counter, 1u);
+        if (threadIdx.x == 0) s_blk = fb_next;
         __syncthreads();
         const uint32_t fb = s_blk;
         if (fb >= A.total_blocks) break;
-        // locate slot (few slots: linear scan)
-        uint32_t s = 0;
-        while (s + 1 < A.nslots && A.jobs[s + 1].block_prefix <= fb) ++s;
-        const SegJob J = A.jobs[s];
-        const uint32_t b = fb - J.block_prefix;
-        const bool low = b < J.b1;
-        const uint64_t q_w = low ? 1ull : J.qbase + 2ull * (uint64_t)(b - J.b1) * E;
-        const uint32_t B = low ? 0u : (b - J.b1) * E;
+        if (threadIdx.x == 0) fb_next = atomicAdd(A.block_counter, 1u);
+        const BlockInfo I = block_info(A, fb);
+        sieve_block(A, tile, pat, I, threadIdx.x, 0);
+        __syncthreads();
+        check_block<PMIN>(A, tile, pmr, I, threadIdx.x, 0, s_red, &s_key, s_q);
+    }
+}
 
-        // ---- K2: sieve the window
-        presieve_window(tile, pat, q_w);
-        __syncthreads();
-        presieve_fixup(tile, q_w);
-        strike_verify(tile, A.pmc + (size_t)s * A.np, A.iA1 - A.iA0, A.iW1 - A.iA0, A.iB1 - A.iA0, B, low);
-        __syncthreads();
-        if (A.qg != nullptr && !low && J.qg_words) {
-            const uint32_t* g = A.qg + s * A.qg_stride_words + B / 32;
-            uint32_t lim = min((uint32_t)TILE_WORDS, J.qg_words - B / 32);
-            for (uint32_t wd = threadIdx.x; wd < lim; wd += blockDim.x) tile[wd] &= __ldg(g + wd);
-            __syncthreads();
-        }
+// Warp-specialised fused kernel: one 1024-thread CTA per SM, two tile
+// buffers.  Warps 0-15 (the sieve group) sieve block k into buffer k & 1
+// while warps 16-31 (the check group) check block k - 1 in the other buffer.
+// Named barriers hand buffers over: FULL[b] (sieve arrives, check waits)
+// and EMPTY[b] (check arrives, sieve waits), so the atomic-heavy sieve and
+// the ALU-heavy check overlap instead of alternating at CTA barriers.
+constexpr int BAR_S = 1, BAR_C = 2, BAR_FULL = 3, BAR_EMPTY = 5; // FULL/EMPTY + buffer
+constexpr uint32_t WS_TILE_STRIDE = TILE_WORDS + 4;
 
-        // ---- K3: minimal p per even, while the tile is in shared memory
-        const uint32_t i0 = b * E;
-        const uint32_t ne = min(E, J.evens - i0);
-        const uint64_t n_first = J.a + 2ull * i0, n_last = n_first + 2ull * (ne - 1);
-        const bool inject_here = (A.inject & 1) == 0 && A.inject >= n_first && A.inject <= n_last;
-        // fast blocks: every even has all NWIN windows valid (n >= 8196,
-        // p_small >= 8193), no n = 4, no injected even
-        const bool fast = !low && jlim_small >= (uint32_t)JH - 1 && !inject_here;
-        K3Acc acc;
-        const uint32_t nw = fast ? ne >> 5 : 0; // full words of the fast path
-        if (fast) {
-            uint32_t* q = s_q[warp];
-            uint32_t qn = 0;  // warp-uniform queue length (< 32 between words)
-            uint32_t sp32 = 0; // sum p of the bit-sliced evens (< 2^32 per lane)
-            // sum p * (bit index) is deferred: z planes and found bits of up
-            // to VACC words are summed per bit position as bit-sliced
-            // counters V (z) and FC (found), then reduced by bit index once
-            uint32_t V[VPL], FC[FPL];
-#pragma unroll
-            for (int k = 0; k < VPL; ++k) V[k] = 0;
-#pragma unroll
-            for (int k = 0; k < FPL; ++k) FC[k] = 0;
-            uint32_t nacc = 0;
-            for (uint32_t wb = warp * 32; wb < nw; wb += THREADS) {
-                const uint32_t w = wb + lane;
-                uint32_t U = 0;
-                if (w < nw) {
-                    uint32_t Z[NPL];
-                    U = scan_word(tile, w, Z);
-                    const uint32_t F = ~U;
-                    // p = 3 + 2z: sum p of the word (weight 32w below)
-                    uint32_t P = 3 * __popc(F);
-#pragma unroll
-                    for (int bp = 0; bp < NPL; ++bp) P += (2u << bp) * __popc(Z[bp]);
-                    sp32 += P;
-                    acc.spi += (uint64_t)(32 * w) * P;
-                    // V += Z, FC += F (ripple-carry, bit-sliced)
-                    uint32_t cy = V[0] & Z[0];
-                    V[0] ^= Z[0];
-#pragma unroll
-                    for (int bp = 1; bp < NPL; ++bp) {
-                        const uint32_t v = V[bp], z = Z[bp];
-                        V[bp] = v ^ z ^ cy;
-                        cy = (v & z) | (cy & (v ^ z));
-                    }
-#pragma unroll
-                    for (int bp = NPL; bp < VPL; ++bp) {
-                        const uint32_t v = V[bp];
-                        V[bp] = v ^ cy;
-                        cy = v & cy;
-                    }
-                    cy = F;
-#pragma unroll
-                    for (int k = 0; k < FPL; ++k) {
-                        const uint32_t f = FC[k];
-                        FC[k] = f ^ cy;
-                        cy = f & cy;
-                    }
-                    if constexpr (PMIN) {
-                        for (uint32_t i = 0; i < 32; ++i) {
-                            if (!((F >> i) & 1)) continue;
-                            uint32_t z = 0;
-#pragma unroll
-                            for (int bp = 0; bp < NPL; ++bp) z |= ((Z[bp] >> i) & 1) << bp;
-                            A.pmin_out[i0 + 32 * w + i] = 3 + 2 * z;
-                        }
-                    }
-                }
-                if (++nacc == VACC) {
-                    acc.spi += vsum_by_index(V, FC);
-                    nacc = 0;
-                }
-                // deep evens: compact into the warp queue, drain 32 at a time
-                const uint32_t c = __popc(U);
-                uint32_t incl = c;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= (uint32_t)o) incl += y;
-                }
-                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-                if (qn + total <= QCAP) {
-                    uint32_t pos = qn + incl - c;
-                    while (U) {
-                        const uint32_t bit = __ffs(U) - 1;
-                        U &= U - 1;
-                        q[pos++] = (32 * w + bit) | ((ZBS / 64) << 24);
-                    }
-                    qn += total;
-                    __syncwarp();
-                    while (qn >= 32) qn = deep_round<PMIN>(tile, pmr, q, qn, 32, lane, i0, s, J, A, jlim_small, acc);
-                } else {
-                    while (U) { // queue full: this lane's deep evens in place
-                        const uint32_t bit = __ffs(U) - 1;
-                        U &= U - 1;
-                        deep_even<PMIN>(tile, pmr, 32 * w + bit, i0, s, J, A, jlim_small, acc);
-                    }
-                    __syncwarp();
-                }
+template <bool PMIN>
+__global__ void __launch_bounds__(2 * THREADS, 1) k_verify_ws(VerifyArgs A) {
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t* tiles = smem;                                 // 2 x WS_TILE_STRIDE
+    uint32_t* pat = smem + WS_PAT_OFF;                      // PAT_WORDS
+    uint64_t* pmr = (uint64_t*)(smem + WS_PMR_OFF);         // NWIN
+    __shared__ uint32_t s_fb[2];
+    __shared__ unsigned long long s_red[NWARPS][3];
+    __shared__ unsigned long long s_key;
+    __shared__ uint32_t s_q[NWARPS][QCAP];
+
+    for (uint32_t i = threadIdx.x; i < PAT_WORDS; i += blockDim.x) pat[i] = A.gpat[i];
+    for (uint32_t i = threadIdx.x; i < (uint32_t)NWIN; i += blockDim.x) pmr[i] = A.pmr[i];
+    for (uint32_t i = threadIdx.x; i < 8; i += blockDim.x) tiles[(i >> 2) * WS_TILE_STRIDE + TILE_WORDS + (i & 3)] = 0;
+    __syncthreads();
+    const int NB = 2 * THREADS; // participants of FULL / EMPTY
+    if (threadIdx.x < THREADS) {
+        // ---- sieve group
+        const uint32_t tid = threadIdx.x;
+        uint32_t fb_next = 0;
+        if (tid == 0) fb_next = atomicAdd(A.block_counter, 1u);
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t bs = k & 1;
+            uint32_t* tile = tiles + bs * WS_TILE_STRIDE;
+            if (k >= 2) nb_sync(BAR_EMPTY + bs, NB); // check group done with block k - 2
+            if (tid == 0) s_fb[bs] = fb_next;
+            gbar(BAR_S);
+            const uint32_t fb = s_fb[bs];
+            if (fb >= A.total_blocks) {
+                if (k >= 1) nb_sync(BAR_EMPTY + (bs ^ 1), NB); // absorb the last EMPTY
+                nb_arrive(BAR_FULL + bs, NB);                  // check group sees the end
+                return;
             }
-            while (qn) qn = deep_round<PMIN>(tile, pmr, q, qn, min(qn, 32u), lane, i0, s, J, A, jlim_small, acc);
-            if (nacc) acc.spi += vsum_by_index(V, FC);
-            acc.sp += sp32;
+            if (tid == 0) fb_next = atomicAdd(A.block_counter, 1u);
+            const BlockInfo I = block_info(A, fb);
+            sieve_block(A, tile, pat, I, tid, BAR_S);
+            nb_arrive(BAR_FULL + bs, NB);
         }
-        {
-            // generic path (whole block, or the tail of a fast block)
-            const uint32_t t0 = low ? (uint32_t)((J.a - 4) >> 1) : (uint32_t)JH;
-            for (uint32_t il = 32 * nw + threadIdx.x; il < ne; il += blockDim.x)
-                generic_even<PMIN>(tile, pmr, il, t0, i0, s, J, A, jlim_small, acc);
+    } else {
+        // ---- check group
+        const uint32_t tid = threadIdx.x - THREADS;
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t bs = k & 1;
+            nb_sync(BAR_FULL + bs, NB);
+            const uint32_t fb = s_fb[bs];
+            if (fb >= A.total_blocks) return;
+            const BlockInfo I = block_info(A, fb);
+            check_block<PMIN>(A, tiles + bs * WS_TILE_STRIDE, pmr, I, tid, BAR_C, s_red, &s_key, s_q);
+            nb_arrive(BAR_EMPTY + bs, NB);
         }
-        // ---- block reduction -> slot accumulators; key = p << 32 | ~iseg
-        uint64_t key = acc.mp ? (((uint64_t)acc.mp << 32) | (0xFFFFFFFFu - (i0 + acc.mi))) : 0;
-        uint64_t sp64 = acc.sp, spi = acc.spi + (uint64_t)i0 * acc.sp;
-        for (int o = 16; o; o >>= 1) {
-            sp64 += __shfl_xor_sync(0xffffffffu, sp64, o);
-            spi += __shfl_xor_sync(0xffffffffu, spi, o);
-            const uint64_t ok = __shfl_xor_sync(0xffffffffu, key, o);
-            key = ok > key ? ok : key;
-        }
-        if (lane == 0) {
-            s_red[warp][0] = sp64;
-            s_red[warp][1] = spi;
-            s_red[warp][2] = key;
-        }
-        __syncthreads();
-        if (threadIdx.x == 0) {
-            uint64_t S = 0, SPI = 0, K = 0;
-            for (int w = 0; w < NWARPS; ++w) {
-                S += s_red[w][0];
-                SPI += s_red[w][1];
-                K = s_red[w][2] > K ? s_red[w][2] : K;
-            }
-            atomicAdd(&A.acc[s].sum, (unsigned long long)S);
-            atomicAdd(&A.acc[s].hash, (unsigned long long)((J.a >> 1) * S + SPI));
-            s_key = K;
-        }
-        __syncthreads();
-        uint64_t K = s_key;
-        if (nw && K < ((uint64_t)(3 + 2 * ZBS) << 32)) {
-            // no deep even beat the bit-sliced range: the block max may be a
-            // bit-sliced even -- rescan for max z (smallest il on ties)
-            uint32_t bz = 0, bi = 0xFFFFFFFFu;
-            for (uint32_t wb = warp * 32; wb < nw; wb += THREADS) {
-                const uint32_t w = wb + lane;
-                if (w >= nw) continue;
-                uint32_t Z[NPL];
-                uint32_t cand = ~scan_word(tile, w, Z);
-                if (!cand) continue;
-                uint32_t mz = 0;
-#pragma unroll
-                for (int bp = NPL - 1; bp >= 0; --bp) {
-                    const uint32_t t = cand & Z[bp];
-                    if (t) {
-                        cand = t;
-                        mz |= 1u << bp;
-                    }
-                }
-                const uint32_t il = 32 * w + __ffs(cand) - 1;
-                if (bi == 0xFFFFFFFFu || mz > bz) { // words ascend per lane: ties keep the smaller il
-                    bz = mz;
-                    bi = il;
-                }
-            }
-            uint64_t kf = bi != 0xFFFFFFFFu ? (((uint64_t)(3 + 2 * bz) << 32) | (0xFFFFFFFFu - (i0 + bi))) : 0;
-            for (int o = 16; o; o >>= 1) {
-                const uint64_t ok = __shfl_xor_sync(0xffffffffu, kf, o);
-                kf = ok > kf ? ok : kf;
-            }
-            if (lane == 0) atomicMax(&s_key, (unsigned long long)kf);
-            __syncthreads();
-            K = s_key;
-        }
-        if (threadIdx.x == 0 && K) atomicMax(&A.acc[s].key, (unsigned long long)K);
     }
 }
 
@@ -1084,10 +1195,17 @@ cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint3
     return cudaGetLastError();
 }
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st) {
+#if GB_WS
+    if (a.pmin_out)
+        k_verify_ws<true><<<grid, 2 * THREADS, WS_SMEM, st>>>(a);
+    else
+        k_verify_ws<false><<<grid, 2 * THREADS, WS_SMEM, st>>>(a);
+#else
     if (a.pmin_out)
         k_verify_blocks<true><<<grid, THREADS, VERIFY_SMEM, st>>>(a);
     else
         k_verify_blocks<false><<<grid, THREADS, VERIFY_SMEM, st>>>(a);
+#endif
     return cudaGetLastError();
 }
 cudaError_t launch_stragglers(const SegJob* jobs, const StragEntry* list, const unsigned int* list_count,
@@ -1123,8 +1241,19 @@ int verify_occupancy(int* blocks_per_sm) {
     if (cudaFuncSetAttribute(k_sieve_interval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SIEVE_SMEM) !=
         cudaSuccess)
         return 1;
+#if GB_WS
+    if (cudaFuncSetAttribute(k_verify_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_SMEM) !=
+        cudaSuccess)
+        return 1;
+    if (cudaFuncSetAttribute(k_verify_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_SMEM) !=
+        cudaSuccess)
+        return 1;
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_verify_ws<false>, 2 * THREADS,
+                                                              WS_SMEM);
+#else
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_verify_blocks<false>, THREADS,
                                                               VERIFY_SMEM);
+#endif
 }
 
 } // namespace gbk

@@ -50,6 +50,10 @@ constexpr uint32_t VERIFY_PAT_OFF = TILE_WORDS + 4;
 constexpr uint32_t VERIFY_PMR_OFF = (VERIFY_PAT_OFF + PAT_WORDS + 3) & ~3u; // 16-B aligned, in words
 constexpr size_t VERIFY_SMEM = (size_t)VERIFY_PMR_OFF * 4 + NWIN * 8;
 constexpr size_t SIEVE_SMEM = (TILE_WORDS + 1 + PAT_WORDS) * 4;
+// k_verify_ws dynamic smem: [tile 0 | 4 pad][tile 1 | 4 pad][patterns][pmr]
+constexpr uint32_t WS_PAT_OFF = 2 * (TILE_WORDS + 4);
+constexpr uint32_t WS_PMR_OFF = (WS_PAT_OFF + PAT_WORDS + 3) & ~3u;
+constexpr size_t WS_SMEM = (size_t)WS_PMR_OFF * 4 + NWIN * 8;
 
 // ---- launchers (gb_kernels.cu); all asynchronous on `st`
 cudaError_t launch_init_tables(uint32_t* pat, uint64_t* pmr, uint64_t p_small, cudaStream_t st);
