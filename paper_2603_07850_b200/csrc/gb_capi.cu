@@ -95,6 +95,7 @@ struct gb_dev {
     uint32_t* d_primes = nullptr;
     uint32_t iA0 = 0, iA1 = 0, iB1 = 0; // tile prime index ranges
     uint32_t iW1 = 0;                   // first tile prime >= W
+    uint16_t* d_wsplit = nullptr;       // [NWARPS][32] balanced warp-cooperative primes
     uint64_t iL0 = 0, iL1 = 0;          // large primes
     uint32_t* d_pat = nullptr;
     uint64_t* d_pmr = nullptr;
@@ -235,6 +236,7 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     A.iW1 = d->iW1;
     A.np = np;
     A.pmc = b.d_pmc;
+    A.wsplit = d->d_wsplit;
     A.qg = large ? b.d_qg : nullptr;
     A.qg_stride_words = d->qg_stride;
     A.gpat = d->d_pat;
@@ -492,6 +494,23 @@ static int build_tables(gb_dev* d) {
     d->iW1 = std::max(d->iA1, std::min(d->iB1, (uint32_t)(std::lower_bound(hp.begin(), hp.end(), W) - hp.begin())));
     d->iL0 = d->iB1;
     d->iL1 = total;
+    {
+        // warp-cooperative primes [iA0, iA1) to warps, longest first onto the
+        // least loaded warp (cost ~ strikes per lane W / 32p + setup)
+        std::vector<uint16_t> ws(NWARPS * 32, 0xFFFF);
+        std::vector<double> load(NWARPS, 0.0);
+        std::vector<int> cnt(NWARPS, 0);
+        for (uint32_t i = d->iA0; i < d->iA1; ++i) { // ascending p = descending cost
+            int best = -1;
+            for (int w = 0; w < NWARPS; ++w)
+                if (cnt[w] < 32 && (best < 0 || load[w] < load[best])) best = w;
+            if (best < 0) GB_FAIL(d, GB_ERR_INTERNAL, "too many warp-cooperative primes");
+            ws[best * 32 + cnt[best]++] = (uint16_t)(i - d->iA0);
+            load[best] += (double)W / (32.0 * hp[i]) + 4.0;
+        }
+        CU(d, dmalloc(d->device, &d->d_wsplit, ws.size() * sizeof(uint16_t)));
+        CU(d, cudaMemcpy(d->d_wsplit, ws.data(), ws.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+    }
     CU(d, cudaStreamSynchronize(d->sync.st)); // tables ready before any batch stream
     return GB_OK;
 }
@@ -584,6 +603,7 @@ int gb_close(gb_dev* d) {
     dfree(d->device, d->flush_buf);
     dfree(d->device, d->d_pat);
     dfree(d->device, d->d_pmr);
+    dfree(d->device, d->d_wsplit);
     delete d;
     return GB_OK;
 }

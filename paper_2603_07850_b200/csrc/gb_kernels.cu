@@ -389,7 +389,8 @@ __device__ __forceinline__ void strike_warp(uint32_t* tile, uint32_t o, uint32_t
 // thread per prime above; primes >= W (index >= nW) strike at most once.
 // pmc: this slot's {p, m, d, c0} row (index i - iA0).
 __device__ __forceinline__ void strike_verify(uint32_t* tile, const uint4* __restrict__ pmc, uint32_t nA,
-                                              uint32_t nW, uint32_t nB, uint32_t B, bool low, uint32_t tid) {
+                                              uint32_t nW, uint32_t nB, uint32_t B, bool low, uint32_t tid,
+                                              const uint16_t* __restrict__ wsplit) {
     const uint32_t lane = tid & 31, warp = tid >> 5;
     if (low) {
         for (uint32_t i = warp; i < nA; i += NWARPS) {
@@ -404,12 +405,14 @@ __device__ __forceinline__ void strike_verify(uint32_t* tile, const uint4* __res
         return;
     }
     {
-        // warp-cooperative primes warp, warp + NWARPS, ...: the lanes load
+        // warp-cooperative primes: warp w takes the rows wsplit[w][0..] (the
+        // host balances sum W/p over warps, longest first); the lanes load
         // the rows and compute the offsets in parallel, then stride in turn
-        const uint32_t nmine = warp < nA ? (nA - warp + NWARPS - 1) / NWARPS : 0; // <= 32
+        const uint32_t idx = wsplit[warp * 32 + lane];
+        const uint32_t nmine = __popc(__ballot_sync(0xffffffffu, idx != 0xFFFFu)); // packed from lane 0
         uint32_t pm = 0, om = W;
-        if (lane < nmine) {
-            const uint4 v = __ldg(pmc + warp + NWARPS * lane);
+        if (idx != 0xFFFFu) {
+            const uint4 v = __ldg(pmc + idx);
             pm = v.x;
             om = block_off(v, B);
         }
@@ -499,7 +502,7 @@ constexpr uint32_t ZBS = 128;
 static_assert(P_WARP_MAX / 2 <= 32 * NWARPS, "warp-cooperative primes: at most 32 per warp");
 static_assert(E < (1u << 24), "deep queue entries pack il in 24 bits");
 constexpr int NPL = BS_SCAN128_PLANES;   // z planes
-constexpr uint32_t QCAP = 160;           // per-warp deep-even queue
+constexpr uint32_t QCAP = 256;           // per-warp deep-even queue
 
 // Straggler entry for an even with no candidate inside the in-tile halo.
 __device__ __forceinline__ void push_straggler(const VerifyArgs& A, const SegJob& J, uint32_t s, uint32_t iseg,
@@ -682,7 +685,7 @@ __device__ __forceinline__ void sieve_block(const VerifyArgs& A, uint32_t* tile,
     gbar(bar);
     presieve_fixup(tile, I.q_w, tid);
     strike_verify(tile, A.pmc + (size_t)I.s * A.np, A.iA1 - A.iA0, A.iW1 - A.iA0, A.iB1 - A.iA0, I.B, I.low,
-                  tid);
+                  tid, A.wsplit);
     if (A.qg != nullptr && !I.low && I.J.qg_words) {
         gbar(bar);
         const uint32_t* g = A.qg + I.s * A.qg_stride_words + I.B / 32;
@@ -726,59 +729,64 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
         for (int k = 0; k < VPL; ++k) V[k] = 0;
 #pragma unroll
         for (int k = 0; k < FPL; ++k) FC[k] = 0;
-        uint32_t nacc = 0;
-        for (uint32_t wb = warp * 32; wb < nw; wb += THREADS) {
-            const uint32_t w = wb + lane;
-            uint32_t U = 0;
-            if (w < nw) {
-                uint32_t Z[NPL];
-                U = scan_word(tile, w, Z);
-                const uint32_t F = ~U;
-                // p = 3 + 2z: sum p of the word (weight 32w below)
-                uint32_t P = 3 * __popc(F);
+        // VACC words per lane per step (w = wb + k THREADS + lane): their
+        // vertical counters are reduced and their deep evens compacted once
+        for (uint32_t wb = warp * 32; wb < nw; wb += VACC * THREADS) {
+            uint32_t U[VACC];
 #pragma unroll
-                for (int bp = 0; bp < NPL; ++bp) P += (2u << bp) * __popc(Z[bp]);
-                sp32 += P;
-                acc.spi += (uint64_t)(32 * w) * P;
-                // V += Z, FC += F (ripple-carry, bit-sliced)
-                uint32_t cy = V[0] & Z[0];
-                V[0] ^= Z[0];
+            for (uint32_t k = 0; k < VACC; ++k) {
+                const uint32_t w = wb + k * THREADS + lane;
+                U[k] = 0;
+                if (w < nw) {
+                    uint32_t Z[NPL];
+                    U[k] = scan_word(tile, w, Z);
+                    const uint32_t F = ~U[k];
+                    // p = 3 + 2z: sum p of the word (weight 32w below)
+                    uint32_t P = 3 * __popc(F);
 #pragma unroll
-                for (int bp = 1; bp < NPL; ++bp) {
-                    const uint32_t v = V[bp], z = Z[bp];
-                    V[bp] = v ^ z ^ cy;
-                    cy = (v & z) | (cy & (v ^ z));
-                }
+                    for (int bp = 0; bp < NPL; ++bp) P += (2u << bp) * __popc(Z[bp]);
+                    sp32 += P;
+                    acc.spi += (uint64_t)(32 * w) * P;
+                    // V += Z, FC += F (ripple-carry, bit-sliced)
+                    uint32_t cy = V[0] & Z[0];
+                    V[0] ^= Z[0];
 #pragma unroll
-                for (int bp = NPL; bp < VPL; ++bp) {
-                    const uint32_t v = V[bp];
-                    V[bp] = v ^ cy;
-                    cy = v & cy;
-                }
-                cy = F;
+                    for (int bp = 1; bp < NPL; ++bp) {
+                        const uint32_t v = V[bp], z = Z[bp];
+                        V[bp] = v ^ z ^ cy;
+                        cy = (v & z) | (cy & (v ^ z));
+                    }
 #pragma unroll
-                for (int k = 0; k < FPL; ++k) {
-                    const uint32_t f = FC[k];
-                    FC[k] = f ^ cy;
-                    cy = f & cy;
-                }
-                if constexpr (PMIN) {
-                    for (uint32_t i = 0; i < 32; ++i) {
-                        if (!((F >> i) & 1)) continue;
-                        uint32_t z = 0;
+                    for (int bp = NPL; bp < VPL; ++bp) {
+                        const uint32_t v = V[bp];
+                        V[bp] = v ^ cy;
+                        cy = v & cy;
+                    }
+                    cy = F;
 #pragma unroll
-                        for (int bp = 0; bp < NPL; ++bp) z |= ((Z[bp] >> i) & 1) << bp;
-                        A.pmin_out[i0 + 32 * w + i] = 3 + 2 * z;
+                    for (int kk = 0; kk < FPL; ++kk) {
+                        const uint32_t f = FC[kk];
+                        FC[kk] = f ^ cy;
+                        cy = f & cy;
+                    }
+                    if constexpr (PMIN) {
+                        for (uint32_t i = 0; i < 32; ++i) {
+                            if (!((F >> i) & 1)) continue;
+                            uint32_t z = 0;
+#pragma unroll
+                            for (int bp = 0; bp < NPL; ++bp) z |= ((Z[bp] >> i) & 1) << bp;
+                            A.pmin_out[i0 + 32 * w + i] = 3 + 2 * z;
+                        }
                     }
                 }
             }
-            if (++nacc == VACC) {
-                acc.spi += vsum_by_index(V, FC);
-                nacc = 0;
-            }
-            // deep evens: compact into the warp queue, drain 32 at a time
-            const uint32_t c = __popc(U);
-            uint32_t incl = c;
+            acc.spi += vsum_by_index(V, FC);
+            // deep evens of the VACC words: compact into the warp queue with
+            // one warp prefix sum, drain 32 at a time
+            uint32_t cnt = 0;
+#pragma unroll
+            for (uint32_t k = 0; k < VACC; ++k) cnt += __popc(U[k]);
+            uint32_t incl = cnt;
 #pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
                 const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
@@ -786,26 +794,33 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
             }
             const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
             if (qn + total <= QCAP) {
-                uint32_t pos = qn + incl - c;
-                while (U) {
-                    const uint32_t bit = __ffs(U) - 1;
-                    U &= U - 1;
-                    q[pos++] = (32 * w + bit) | ((ZBS / 64) << 24);
+                uint32_t pos = qn + incl - cnt;
+#pragma unroll
+                for (uint32_t k = 0; k < VACC; ++k) {
+                    const uint32_t w = wb + k * THREADS + lane;
+                    while (U[k]) {
+                        const uint32_t bit = __ffs(U[k]) - 1;
+                        U[k] &= U[k] - 1;
+                        q[pos++] = (32 * w + bit) | ((ZBS / 64) << 24);
+                    }
                 }
                 qn += total;
                 __syncwarp();
                 while (qn >= 32) qn = deep_round<PMIN>(tile, pmr, q, qn, 32, lane, i0, s, J, A, jlim_small, acc);
             } else {
-                while (U) { // queue full: this lane's deep evens in place
-                    const uint32_t bit = __ffs(U) - 1;
-                    U &= U - 1;
-                    deep_even<PMIN>(tile, pmr, 32 * w + bit, i0, s, J, A, jlim_small, acc);
+#pragma unroll
+                for (uint32_t k = 0; k < VACC; ++k) { // queue full: this lane's deep evens in place
+                    const uint32_t w = wb + k * THREADS + lane;
+                    while (U[k]) {
+                        const uint32_t bit = __ffs(U[k]) - 1;
+                        U[k] &= U[k] - 1;
+                        deep_even<PMIN>(tile, pmr, 32 * w + bit, i0, s, J, A, jlim_small, acc);
+                    }
                 }
                 __syncwarp();
             }
         }
         while (qn) qn = deep_round<PMIN>(tile, pmr, q, qn, min(qn, 32u), lane, i0, s, J, A, jlim_small, acc);
-        if (nacc) acc.spi += vsum_by_index(V, FC);
         acc.sp += sp32;
     }
     {

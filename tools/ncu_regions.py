@@ -41,21 +41,28 @@ def line_map(obj, kernel):
         subprocess.run(["cuobjdump", "-xelf", "all", os.path.abspath(obj)], cwd=td, check=True,
                        capture_output=True)
         cubins = [os.path.join(td, f) for f in os.listdir(td) if f.endswith(".cubin")]
-        text = subprocess.run(["nvdisasm", "-g", "-c", cubins[0]], capture_output=True, text=True,
+        text = subprocess.run(["nvdisasm", "-gi", "-c", cubins[0]], capture_output=True, text=True,
                               check=True).stdout
     m = {}
     cur_fn = None
     loc = None
+    fresh = True  # -gi prints the inlining chain innermost first: keep the first line
     for ln in text.splitlines():
         s = ln.strip()
         if s.startswith(".text."):
             cur_fn = s[len(".text."):].rstrip(":")
             continue
-        mm = re.match(r'//## File "([^"]+)", line (\d+)', s)
+        mm = re.match(r'//## File "([^"]+)", line (\d+)(?: inlined at "([^"]+)", line (\d+))?', s)
         if mm:
-            loc = (os.path.basename(mm.group(1)), int(mm.group(2)))
+            if fresh:
+                loc = (os.path.basename(mm.group(1)), int(mm.group(2)))
+                if mm.group(3):  # innermost line + its call site
+                    loc = loc + (os.path.basename(mm.group(3)), int(mm.group(4)))
+                fresh = False
             continue
         mo = re.match(r"/\*([0-9a-f]{4,})\*/", s)
+        if mo:
+            fresh = True
         if mo and cur_fn and kernel in cur_fn and loc:
             m.setdefault(cur_fn, {})[int(mo.group(1), 16)] = loc
     return m
@@ -76,8 +83,11 @@ def func_spans(src_dir):
     return spans
 
 
+TINY = {"gbar", "nb_sync", "nb_arrive"}  # attribute these to their call site
+
+
 def region_of(spans, loc):
-    f, line = loc
+    f, line = loc[0], loc[1]
     st = spans.get(f, [])
     i = bisect.bisect_right([s for s, _ in st], line) - 1
     return f"{st[i][1]}" if i >= 0 else f"{f}:?"
@@ -106,6 +116,8 @@ def main():
         off = int(r["Address"], 16) - base
         loc = offs.get(off)
         reg = region_of(spans, loc) if loc else "?"
+        if loc and len(loc) > 2 and reg in TINY:
+            reg = f"{reg}@{loc[3]}"
         c = agg[reg]
         samp = int(r["Warp Stall Sampling (All Samples)"] or 0)
         inst = int(r["Instructions Executed"] or 0)
@@ -118,8 +130,8 @@ def main():
             c[h] += v
             tot[h] += v
         if loc:
-            lines[loc]["samples"] += samp
-            lines[loc]["inst"] += inst
+            lines[loc[:2]]["samples"] += samp
+            lines[loc[:2]]["inst"] += inst
     print(f"# {a.rep}: {tot['samples']} stall samples, {tot['inst']:,} warp-instructions")
     print(f"{'region':28s} {'samples':>8s} {'%':>6s} {'inst%':>6s}  top stalls")
     for reg, c in sorted(agg.items(), key=lambda kv: -kv[1]["samples"]):
