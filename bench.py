@@ -18,7 +18,7 @@ single-GPU 36.5 s headline); `--limit 1e13` is C4.
            gb_open (K1 base primes on the device) + pool drain + records
            back to the host + close + the final all-gather; h2d/d2h bytes
            are the job descriptors and records that cross PCIe.
-`roofline`: the fused sieve+check kernel (k_verify_blocks), algorithmic
+`roofline`: the fused sieve+check kernel (k_verify_ws), algorithmic
            shared-memory bytes per launch (SURVEY.md sec. 8d frozen formula
            B(N) = 4 S(sqrt N) + 16 W64(N) + 0.25 B per even) / its average
            launch duration, against the shared-memory bandwidth measured live
@@ -367,7 +367,7 @@ def main():
     traffic = per_even * evens_timed_rank / max(verify_launches, 1) if per_even else None
     peaks = load_json(os.path.join(ROOT, "MEASURED_PEAKS.json")) or {}
     roofline = {
-        "bound": "smem", "kernel": "k_verify_blocks (fused K2 sieve + K3 check)",
+        "bound": "smem", "kernel": "k_verify_ws (fused K2 sieve + K3 check, warp-specialised)",
         "achieved": achieved_gbs, "peak": peak_gbs, "unit": "GB/s",
         "frac": (achieved_gbs / peak_gbs) if achieved_gbs and peak_gbs else None,
         "traffic": traffic,
@@ -419,6 +419,8 @@ def main():
                        "segments": merged["segments"]},
             "wall_seconds_per_pass": total_ms / args.steps / 1e3,
             "paper_rtx5090_seconds": {10**12: 36.5116, 10**13: 133.5}.get(args.limit),
+            "paper_note": {10**12: "1x RTX 5090 (PAPER.md:454)",
+                           10**13: "4x RTX 5090 (PAPER.md:455)"}.get(args.limit),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "seconds_per_step": sum(e2e_s) / args.steps},
             "gpu_launches": launches,

@@ -13,6 +13,7 @@
 #include <chrono>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <mutex>
@@ -553,14 +554,18 @@ int gb_open(int device, const gb_params* params, gb_dev** out) {
             rc = GB_ERR_CUDA;
             break;
         }
-        cudaDeviceProp prop;
-        cudaGetDeviceProperties(&prop, device);
-        if (prop.major != 10) {
-            set_err(d, std::string("gb_open: built for sm_100a, device is ") + prop.name);
+        // two attributes, not cudaGetDeviceProperties (which queries them all
+        // and costs up to ~100 ms per call)
+        int major = 0, minor = 0;
+        cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, device);
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, device);
+        if (major != 10 || minor != 0) {
+            set_err(d, "gb_open: built for sm_100a, device is sm_" + std::to_string(major) + std::to_string(minor));
             rc = GB_ERR_CUDA;
             break;
         }
-        d->sms = prop.multiProcessorCount;
+        cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, device);
+        const double t_open0 = now_s();
         int occ = 0;
         if (verify_occupancy(&occ) != 0 || occ < 1) {
             set_err(d, "gb_open: fused kernel cannot be resident (shared memory)");
@@ -574,12 +579,17 @@ int gb_open(int device, const gb_params* params, gb_dev** out) {
             rc = GB_ERR_CUDA;
             break;
         }
+        const double t_open1 = now_s();
         if ((rc = build_tables(d)) != GB_OK) break;
+        const double t_open2 = now_s();
         d->max_piece = std::min<uint64_t>(d->prm.max_seg_evens, MAX_PIECE);
         uint64_t blocks = (d->max_piece + E - 1) / E;
         d->qg_stride = (blocks * E + JH + 31) / 32;
         if ((rc = batch_alloc(d, d->sync, true)) != GB_OK) break;
         for (int i = 0; i < NBATCH && rc == GB_OK; ++i) rc = batch_alloc(d, d->batches[i], true);
+        if (getenv("GB_DEBUG_OPEN"))
+            fprintf(stderr, "gb_open: setup %.1f ms, tables %.1f ms, batches %.1f ms\n", 1e3 * (t_open1 - t_open0),
+                    1e3 * (t_open2 - t_open1), 1e3 * (now_s() - t_open2));
     } while (false);
     if (rc != GB_OK) {
         t_err = d->err;

@@ -16,7 +16,7 @@ timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --lo
 timeout 900 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file $O/launches_bench.csv \
   python bench.py --limit 1e11 --steps 1 --warmup 3 --no-cpu-baseline > $O/launches_bench.log 2>&1
 fi
-timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_verify_blocks -s 1 -c 1 \
+timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_verify -s 1 -c 1 \
   -o $O/prof_verify -f python tools/profile_one.py 1e12 9 > $O/ncu_full.log 2>&1
 fi
 ls -la $O

@@ -108,7 +108,7 @@ def main():
         rows = ncu_csv(a.rep, "--page", "raw")
         hdr, units, vals = rows[0], rows[1], rows[2]
         m = {h: (vals[i], units[i]) for i, h in enumerate(hdr)}
-        txt = [f"# ncu --set full --clock-control none --import-source on -k regex:k_verify_blocks "
+        txt = [f"# ncu --set full --clock-control none --import-source on -k regex:k_verify "
                f"({os.path.basename(a.rep)}) {a.note}"]
         for k in METRICS:
             if k in m:
