@@ -498,12 +498,12 @@ static int build_tables(gb_dev* d) {
     {
         // warp-cooperative primes [iA0, iA1) to warps, longest first onto the
         // least loaded warp (cost ~ strikes per lane W / 32p + setup)
-        std::vector<uint16_t> ws(NWARPS * 32, 0xFFFF);
-        std::vector<double> load(NWARPS, 0.0);
-        std::vector<int> cnt(NWARPS, 0);
+        std::vector<uint16_t> ws(SPLIT_WARPS * 32, 0xFFFF);
+        std::vector<double> load(SPLIT_WARPS, 0.0);
+        std::vector<int> cnt(SPLIT_WARPS, 0);
         for (uint32_t i = d->iA0; i < d->iA1; ++i) { // ascending p = descending cost
             int best = -1;
-            for (int w = 0; w < NWARPS; ++w)
+            for (int w = 0; w < SPLIT_WARPS; ++w)
                 if (cnt[w] < 32 && (best < 0 || load[w] < load[best])) best = w;
             if (best < 0) GB_FAIL(d, GB_ERR_INTERNAL, "too many warp-cooperative primes");
             ws[best * 32 + cnt[best]++] = (uint16_t)(i - d->iA0);

@@ -28,6 +28,19 @@ constexpr int TILE_WORDS = W / 32;      // u32 words of the window
 constexpr int THREADS = W_LOG2 >= 20 ? 1024 : 512; // threads per CTA of the fused kernel
 constexpr int CTAS_PER_SM = W_LOG2 >= 20 ? 1 : 2;
 constexpr int NWARPS = THREADS / 32;
+// Warp-specialised fused kernel (k_verify_ws): one CTA of WS_THREADS per SM,
+// WS_ST sieve threads + WS_CT check threads.
+#ifndef GB_WS
+#define GB_WS 1
+#endif
+#ifndef GB_WS_SIEVE_WARPS
+#define GB_WS_SIEVE_WARPS 16
+#endif
+constexpr int WS_THREADS = 1024;
+constexpr int WS_ST = 32 * GB_WS_SIEVE_WARPS;
+constexpr int WS_CT = WS_THREADS - WS_ST;
+// warps of the group that runs the warp-cooperative strikes
+constexpr int SPLIT_WARPS = GB_WS ? WS_ST / 32 : NWARPS;
 constexpr uint32_t P_TILE_MAX = 1u << 22; // base primes above: K_large (global strikes)
 constexpr uint32_t P_WARP_MAX = 1024;     // primes below: warp-cooperative strikes
 constexpr uint32_t FIRST_STRIKE_P = 53;   // primes below are in the presieve patterns

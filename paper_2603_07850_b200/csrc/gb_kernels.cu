@@ -22,9 +22,6 @@
 #include <algorithm>
 #include <cstdio>
 
-#ifndef GB_WS
-#define GB_WS 1   // warp-specialised fused kernel (sieve and check warp groups, 2 tiles)
-#endif
 
 namespace gbk {
 
@@ -384,21 +381,22 @@ __device__ __forceinline__ void strike_warp(uint32_t* tile, uint32_t o, uint32_t
     for (; wi < (uint32_t)TILE_WORDS; wi += p) atomicAnd(&tile[wi], mask);
 }
 
-// K2 strikes of one verify block by a group of THREADS threads (tid = the
+// K2 strikes of one verify block by a group of GT threads (tid = the
 // thread's index in the group): warp-cooperative below P_WARP_MAX, one
 // thread per prime above; primes >= W (index >= nW) strike at most once.
 // pmc: this slot's {p, m, d, c0} row (index i - iA0).
+template <int GT>
 __device__ __forceinline__ void strike_verify(uint32_t* tile, const uint4* __restrict__ pmc, uint32_t nA,
                                               uint32_t nW, uint32_t nB, uint32_t B, bool low, uint32_t tid,
                                               const uint16_t* __restrict__ wsplit) {
     const uint32_t lane = tid & 31, warp = tid >> 5;
     if (low) {
-        for (uint32_t i = warp; i < nA; i += NWARPS) {
+        for (uint32_t i = warp; i < nA; i += GT / 32) {
             const uint32_t p = __ldg(&pmc[i].x);
             const uint32_t o = low_off(p);
             if (o < W) strike_warp(tile, o, p, lane);
         }
-        for (uint32_t i = nA + tid; i < nB; i += THREADS) {
+        for (uint32_t i = nA + tid; i < nB; i += GT) {
             const uint32_t p = __ldg(&pmc[i].x);
             strike_run(tile, low_off(p), p);
         }
@@ -426,31 +424,31 @@ __device__ __forceinline__ void strike_verify(uint32_t* tile, const uint4* __res
     // are issued before their strikes to keep several in flight per warp
     const uint4* q = pmc + nA + tid;
     const uint4* qe = pmc + nW;
-    for (; q + 3 * THREADS < qe; q += 4 * THREADS) {
-        const uint4 v0 = __ldg(q), v1 = __ldg(q + THREADS), v2 = __ldg(q + 2 * THREADS),
-                    v3 = __ldg(q + 3 * THREADS);
+    for (; q + 3 * GT < qe; q += 4 * GT) {
+        const uint4 v0 = __ldg(q), v1 = __ldg(q + GT), v2 = __ldg(q + 2 * GT),
+                    v3 = __ldg(q + 3 * GT);
         strike_run(tile, block_off(v0, B), v0.x);
         strike_run(tile, block_off(v1, B), v1.x);
         strike_run(tile, block_off(v2, B), v2.x);
         strike_run(tile, block_off(v3, B), v3.x);
     }
-    for (; q < qe; q += THREADS) {
+    for (; q < qe; q += GT) {
         const uint4 v = __ldg(q);
         strike_run(tile, block_off(v, B), v.x);
     }
     q = pmc + nW + tid;
     qe = pmc + nB;
-    for (; q + 7 * THREADS < qe; q += 8 * THREADS) {
+    for (; q + 7 * GT < qe; q += 8 * GT) {
         uint4 v[8];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldg(q + u * THREADS);
+        for (int u = 0; u < 8; ++u) v[u] = __ldg(q + u * GT);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
             const uint32_t o = block_off(v[u], B);
             if (o < W) strike(tile, o);
         }
     }
-    for (; q < qe; q += THREADS) {
+    for (; q < qe; q += GT) {
         const uint4 v = __ldg(q);
         const uint32_t o = block_off(v, B);
         if (o < W) strike(tile, o);
@@ -499,7 +497,7 @@ struct K3Acc {
 // evens per lane (gb_bitslice.cuh); the few evens left ("deep") continue
 // per even from window ZBS/64.
 constexpr uint32_t ZBS = 128;
-static_assert(P_WARP_MAX / 2 <= 32 * NWARPS, "warp-cooperative primes: at most 32 per warp");
+
 static_assert(E < (1u << 24), "deep queue entries pack il in 24 bits");
 constexpr int NPL = BS_SCAN128_PLANES;   // z planes
 constexpr uint32_t QCAP = 256;           // per-warp deep-even queue
@@ -650,8 +648,9 @@ __device__ __forceinline__ uint32_t scan_word(const uint32_t* tile, uint32_t w, 
     return U;
 }
 
-// Barrier of one group of THREADS threads (id 0 = the whole 512-thread CTA).
-__device__ __forceinline__ void gbar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(THREADS) : "memory"); }
+// Barrier of one group of GT threads (id 0 with GT = the CTA size: __syncthreads).
+template <int GT>
+__device__ __forceinline__ void gbar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(GT) : "memory"); }
 __device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 __device__ __forceinline__ void nb_arrive(int id, int n) { asm volatile("bar.arrive %0, %1;" ::"r"(id), "r"(n) : "memory"); }
 
@@ -679,24 +678,25 @@ __device__ __forceinline__ BlockInfo block_info(const VerifyArgs& A, uint32_t fb
 
 // K2: sieve block I into tile by one group (tid = index in the group).  On
 // return this thread's strikes are issued; the caller's barrier publishes.
+template <int GT>
 __device__ __forceinline__ void sieve_block(const VerifyArgs& A, uint32_t* tile, const uint32_t* pat,
                                             const BlockInfo& I, uint32_t tid, int bar) {
-    presieve_window(tile, pat, I.q_w, tid, THREADS);
-    gbar(bar);
+    presieve_window(tile, pat, I.q_w, tid, GT);
+    gbar<GT>(bar);
     presieve_fixup(tile, I.q_w, tid);
-    strike_verify(tile, A.pmc + (size_t)I.s * A.np, A.iA1 - A.iA0, A.iW1 - A.iA0, A.iB1 - A.iA0, I.B, I.low,
+    strike_verify<GT>(tile, A.pmc + (size_t)I.s * A.np, A.iA1 - A.iA0, A.iW1 - A.iA0, A.iB1 - A.iA0, I.B, I.low,
                   tid, A.wsplit);
     if (A.qg != nullptr && !I.low && I.J.qg_words) {
-        gbar(bar);
+        gbar<GT>(bar);
         const uint32_t* g = A.qg + I.s * A.qg_stride_words + I.B / 32;
         const uint32_t lim = min((uint32_t)TILE_WORDS, I.J.qg_words - I.B / 32);
-        for (uint32_t wd = tid; wd < lim; wd += THREADS) tile[wd] &= __ldg(g + wd);
+        for (uint32_t wd = tid; wd < lim; wd += GT) tile[wd] &= __ldg(g + wd);
     }
 }
 
 // K3: minimal p of every even of block I over the sieved tile, by one group;
 // the block's sums / max key go to the slot accumulators.
-template <bool PMIN>
+template <bool PMIN, int GT>
 __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t* tile, const uint64_t* pmr,
                                             const BlockInfo& I, uint32_t tid, int bar,
                                             unsigned long long (*s_red)[3], unsigned long long* s_key_p,
@@ -729,13 +729,13 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
         for (int k = 0; k < VPL; ++k) V[k] = 0;
 #pragma unroll
         for (int k = 0; k < FPL; ++k) FC[k] = 0;
-        // VACC words per lane per step (w = wb + k THREADS + lane): their
+        // VACC words per lane per step (w = wb + k GT + lane): their
         // vertical counters are reduced and their deep evens compacted once
-        for (uint32_t wb = warp * 32; wb < nw; wb += VACC * THREADS) {
+        for (uint32_t wb = warp * 32; wb < nw; wb += VACC * GT) {
             uint32_t U[VACC];
 #pragma unroll
             for (uint32_t k = 0; k < VACC; ++k) {
-                const uint32_t w = wb + k * THREADS + lane;
+                const uint32_t w = wb + k * GT + lane;
                 U[k] = 0;
                 if (w < nw) {
                     uint32_t Z[NPL];
@@ -797,7 +797,7 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
                 uint32_t pos = qn + incl - cnt;
 #pragma unroll
                 for (uint32_t k = 0; k < VACC; ++k) {
-                    const uint32_t w = wb + k * THREADS + lane;
+                    const uint32_t w = wb + k * GT + lane;
                     while (U[k]) {
                         const uint32_t bit = __ffs(U[k]) - 1;
                         U[k] &= U[k] - 1;
@@ -810,7 +810,7 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
             } else {
 #pragma unroll
                 for (uint32_t k = 0; k < VACC; ++k) { // queue full: this lane's deep evens in place
-                    const uint32_t w = wb + k * THREADS + lane;
+                    const uint32_t w = wb + k * GT + lane;
                     while (U[k]) {
                         const uint32_t bit = __ffs(U[k]) - 1;
                         U[k] &= U[k] - 1;
@@ -826,7 +826,7 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
     {
         // generic path (whole block, or the tail of a fast block)
         const uint32_t t0 = low ? (uint32_t)((J.a - 4) >> 1) : (uint32_t)JH;
-        for (uint32_t il = 32 * nw + tid; il < ne; il += THREADS)
+        for (uint32_t il = 32 * nw + tid; il < ne; il += GT)
             generic_even<PMIN>(tile, pmr, il, t0, i0, s, J, A, jlim_small, acc);
     }
     // ---- block reduction -> slot accumulators; key = p << 32 | ~iseg
@@ -843,10 +843,10 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
         s_red[warp][1] = spi;
         s_red[warp][2] = key;
     }
-    gbar(bar);
+    gbar<GT>(bar);
     if (tid == 0) {
         uint64_t S = 0, SPI = 0, K = 0;
-        for (int w = 0; w < NWARPS; ++w) {
+        for (int w = 0; w < (GT / 32); ++w) {
             S += s_red[w][0];
             SPI += s_red[w][1];
             K = s_red[w][2] > K ? s_red[w][2] : K;
@@ -855,13 +855,13 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
         atomicAdd(&A.acc[s].hash, (unsigned long long)((J.a >> 1) * S + SPI));
         s_key = K;
     }
-    gbar(bar);
+    gbar<GT>(bar);
     uint64_t K = s_key;
     if (nw && K < ((uint64_t)(3 + 2 * ZBS) << 32)) {
         // no deep even beat the bit-sliced range: the block max may be a
         // bit-sliced even -- rescan for max z (smallest il on ties)
         uint32_t bz = 0, bi = 0xFFFFFFFFu;
-        for (uint32_t wb = warp * 32; wb < nw; wb += THREADS) {
+        for (uint32_t wb = warp * 32; wb < nw; wb += GT) {
             const uint32_t w = wb + lane;
             if (w >= nw) continue;
             uint32_t Z[NPL];
@@ -888,7 +888,7 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
             kf = ok > kf ? ok : kf;
         }
         if (lane == 0) atomicMax(&s_key, (unsigned long long)kf);
-        gbar(bar);
+        gbar<GT>(bar);
         K = s_key;
     }
     if (tid == 0 && K) atomicMax(&A.acc[s].key, (unsigned long long)K);
@@ -920,38 +920,39 @@ __global__ void __launch_bounds__(THREADS, CTAS_PER_SM) k_verify_blocks(VerifyAr
         if (fb >= A.total_blocks) break;
         if (threadIdx.x == 0) fb_next = atomicAdd(A.block_counter, 1u);
         const BlockInfo I = block_info(A, fb);
-        sieve_block(A, tile, pat, I, threadIdx.x, 0);
+        sieve_block<THREADS>(A, tile, pat, I, threadIdx.x, 0);
         __syncthreads();
-        check_block<PMIN>(A, tile, pmr, I, threadIdx.x, 0, s_red, &s_key, s_q);
+        check_block<PMIN, THREADS>(A, tile, pmr, I, threadIdx.x, 0, s_red, &s_key, s_q);
     }
 }
 
 // Warp-specialised fused kernel: one 1024-thread CTA per SM, two tile
-// buffers.  Warps 0-15 (the sieve group) sieve block k into buffer k & 1
-// while warps 16-31 (the check group) check block k - 1 in the other buffer.
-// Named barriers hand buffers over: FULL[b] (sieve arrives, check waits)
-// and EMPTY[b] (check arrives, sieve waits), so the atomic-heavy sieve and
-// the ALU-heavy check overlap instead of alternating at CTA barriers.
+// buffers.  The first WS_ST threads (the sieve group) sieve block k into
+// buffer k & 1 while the other WS_CT threads (the check group) check block
+// k - 1 in the other buffer.  Named barriers hand buffers over: FULL[b]
+// (sieve arrives, check waits) and EMPTY[b] (check arrives, sieve waits), so
+// the atomic-heavy sieve and the ALU-heavy check overlap instead of
+// alternating at CTA barriers.  The split is tuned so neither group waits.
 constexpr int BAR_S = 1, BAR_C = 2, BAR_FULL = 3, BAR_EMPTY = 5; // FULL/EMPTY + buffer
 constexpr uint32_t WS_TILE_STRIDE = TILE_WORDS + 4;
 
 template <bool PMIN>
-__global__ void __launch_bounds__(2 * THREADS, 1) k_verify_ws(VerifyArgs A) {
+__global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t* tiles = smem;                                 // 2 x WS_TILE_STRIDE
     uint32_t* pat = smem + WS_PAT_OFF;                      // PAT_WORDS
     uint64_t* pmr = (uint64_t*)(smem + WS_PMR_OFF);         // NWIN
     __shared__ uint32_t s_fb[2];
-    __shared__ unsigned long long s_red[NWARPS][3];
+    __shared__ unsigned long long s_red[WS_CT / 32][3];
     __shared__ unsigned long long s_key;
-    __shared__ uint32_t s_q[NWARPS][QCAP];
+    __shared__ uint32_t s_q[WS_CT / 32][QCAP];
 
     for (uint32_t i = threadIdx.x; i < PAT_WORDS; i += blockDim.x) pat[i] = A.gpat[i];
     for (uint32_t i = threadIdx.x; i < (uint32_t)NWIN; i += blockDim.x) pmr[i] = A.pmr[i];
     for (uint32_t i = threadIdx.x; i < 8; i += blockDim.x) tiles[(i >> 2) * WS_TILE_STRIDE + TILE_WORDS + (i & 3)] = 0;
     __syncthreads();
-    const int NB = 2 * THREADS; // participants of FULL / EMPTY
-    if (threadIdx.x < THREADS) {
+    const int NB = WS_THREADS; // participants of FULL / EMPTY
+    if (threadIdx.x < WS_ST) {
         // ---- sieve group
         const uint32_t tid = threadIdx.x;
         uint32_t fb_next = 0;
@@ -961,7 +962,7 @@ __global__ void __launch_bounds__(2 * THREADS, 1) k_verify_ws(VerifyArgs A) {
             uint32_t* tile = tiles + bs * WS_TILE_STRIDE;
             if (k >= 2) nb_sync(BAR_EMPTY + bs, NB); // check group done with block k - 2
             if (tid == 0) s_fb[bs] = fb_next;
-            gbar(BAR_S);
+            gbar<WS_ST>(BAR_S);
             const uint32_t fb = s_fb[bs];
             if (fb >= A.total_blocks) {
                 if (k >= 1) nb_sync(BAR_EMPTY + (bs ^ 1), NB); // absorb the last EMPTY
@@ -970,19 +971,19 @@ __global__ void __launch_bounds__(2 * THREADS, 1) k_verify_ws(VerifyArgs A) {
             }
             if (tid == 0) fb_next = atomicAdd(A.block_counter, 1u);
             const BlockInfo I = block_info(A, fb);
-            sieve_block(A, tile, pat, I, tid, BAR_S);
+            sieve_block<WS_ST>(A, tile, pat, I, tid, BAR_S);
             nb_arrive(BAR_FULL + bs, NB);
         }
     } else {
         // ---- check group
-        const uint32_t tid = threadIdx.x - THREADS;
+        const uint32_t tid = threadIdx.x - WS_ST;
         for (uint32_t k = 0;; ++k) {
             const uint32_t bs = k & 1;
             nb_sync(BAR_FULL + bs, NB);
             const uint32_t fb = s_fb[bs];
             if (fb >= A.total_blocks) return;
             const BlockInfo I = block_info(A, fb);
-            check_block<PMIN>(A, tiles + bs * WS_TILE_STRIDE, pmr, I, tid, BAR_C, s_red, &s_key, s_q);
+            check_block<PMIN, WS_CT>(A, tiles + bs * WS_TILE_STRIDE, pmr, I, tid, BAR_C, s_red, &s_key, s_q);
             nb_arrive(BAR_EMPTY + bs, NB);
         }
     }
@@ -1212,9 +1213,9 @@ cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint3
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st) {
 #if GB_WS
     if (a.pmin_out)
-        k_verify_ws<true><<<grid, 2 * THREADS, WS_SMEM, st>>>(a);
+        k_verify_ws<true><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
     else
-        k_verify_ws<false><<<grid, 2 * THREADS, WS_SMEM, st>>>(a);
+        k_verify_ws<false><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
 #else
     if (a.pmin_out)
         k_verify_blocks<true><<<grid, THREADS, VERIFY_SMEM, st>>>(a);
@@ -1263,7 +1264,7 @@ int verify_occupancy(int* blocks_per_sm) {
     if (cudaFuncSetAttribute(k_verify_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_SMEM) !=
         cudaSuccess)
         return 1;
-    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_verify_ws<false>, 2 * THREADS,
+    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_verify_ws<false>, WS_THREADS,
                                                               WS_SMEM);
 #else
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_verify_blocks<false>, THREADS,

@@ -30,7 +30,7 @@ struct VerifyArgs {
     uint32_t iW1;                 // first tile prime >= W (strikes a block at most once)
     uint32_t np;                  // pmc row length (iB1 - iA0)
     const uint4* pmc;             // nslots * np {p, floor(2^32/p), p - 1 - c0, c0}
-    const uint16_t* wsplit;       // [NWARPS][32] warp-cooperative row indices (0xFFFF = none)
+    const uint16_t* wsplit;       // [SPLIT_WARPS][32] warp-cooperative row indices (0xFFFF = none)
     const uint32_t* qg;           // large-prime bitmask (nullptr = none)
     uint64_t qg_stride_words;
     const uint32_t* gpat;
