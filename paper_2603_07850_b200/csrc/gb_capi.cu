@@ -97,6 +97,7 @@ struct gb_dev {
     uint32_t iA0 = 0, iA1 = 0, iB1 = 0; // tile prime index ranges
     uint32_t iW1 = 0;                   // first tile prime >= W
     uint16_t* d_wsplit = nullptr;       // [NWARPS][32] balanced warp-cooperative primes
+    uint64_t* d_m64 = nullptr;          // floor(2^64 / p) per base prime
     uint64_t iL0 = 0, iL1 = 0;          // large primes
     uint32_t* d_pat = nullptr;
     uint64_t* d_pmr = nullptr;
@@ -218,12 +219,12 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     if (b.timed) CU(d, cudaEventRecord(b.ev_l0, st));
     if (large) {
         CU(d, cudaMemsetAsync(b.d_qg, 0xFF, (size_t)n * d->qg_stride * 4, st));
-        CU(d, launch_large_strike(b.d_jobs, n, d->d_primes, d->iL0, d->iL1, b.d_qg, d->qg_stride, st));
+        CU(d, launch_large_strike(b.d_jobs, n, d->d_primes, d->d_m64, d->iL0, d->iL1, b.d_qg, d->qg_stride, st));
         d->launches++;
     }
     const uint32_t np = d->iB1 - d->iA0;
     if (np) {
-        CU(d, launch_segment_offsets(b.d_jobs, n, d->d_primes, d->iA0, np, b.d_pmc, st));
+        CU(d, launch_segment_offsets(b.d_jobs, n, d->d_primes, d->d_m64, d->iA0, np, b.d_pmc, st));
         d->launches++;
     }
     VerifyArgs A{};
@@ -512,6 +513,9 @@ static int build_tables(gb_dev* d) {
         CU(d, dmalloc(d->device, &d->d_wsplit, ws.size() * sizeof(uint16_t)));
         CU(d, cudaMemcpy(d->d_wsplit, ws.data(), ws.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
     }
+    CU(d, dmalloc(d->device, &d->d_m64, std::max<uint64_t>(total, 1) * sizeof(uint64_t)));
+    CU(d, launch_prime_magic64(d->d_primes, total, d->d_m64, d->sync.st));
+    d->launches++;
     CU(d, cudaStreamSynchronize(d->sync.st)); // tables ready before any batch stream
     return GB_OK;
 }
@@ -614,6 +618,7 @@ int gb_close(gb_dev* d) {
     dfree(d->device, d->d_pat);
     dfree(d->device, d->d_pmr);
     dfree(d->device, d->d_wsplit);
+    dfree(d->device, d->d_m64);
     delete d;
     return GB_OK;
 }
@@ -813,10 +818,10 @@ uint64_t gb_estimate_device_bytes(uint64_t cover_limit, uint64_t p_small, uint64
     const uint64_t np_tile = std::min<uint64_t>(np_all, pi_upper(P_TILE_MAX));
     const uint64_t piece = std::min<uint64_t>(max_seg_evens, MAX_PIECE);
     const uint64_t qg = s > P_TILE_MAX ? SLOTS * (((piece + E - 1) / E) * E + JH + 31) / 32 * 4 : 0;
-    const uint64_t per_batch = SLOTS * np_tile * 4 + qg + (uint64_t)LIST_CAP * (sizeof(StragEntry) + sizeof(StragResult)) +
+    const uint64_t per_batch = SLOTS * np_tile * sizeof(uint4) + qg + (uint64_t)LIST_CAP * (sizeof(StragEntry) + sizeof(StragResult)) +
                                SLOTS * (sizeof(SegJob) + sizeof(SlotAcc) + sizeof(DevRecord)) + 64;
-    // base primes + K1 scratch bitmap (transient) + NBATCH + 1 batches
-    return np_all * 4 + (s / 16 + 64) + (uint64_t)(NBATCH + 1) * per_batch;
+    // base primes + their 64-bit magics + K1 scratch bitmap (transient) + NBATCH + 1 batches
+    return np_all * (4 + 8) + (s / 16 + 64) + (uint64_t)(NBATCH + 1) * per_batch;
 }
 
 int gb_device_memory(int device, uint64_t* free_bytes, uint64_t* total_bytes) {

@@ -117,6 +117,21 @@ __host__ __device__ __forceinline__ uint64_t first_cell_u64(uint64_t q_w, uint64
     return d >> 1;
 }
 
+#ifdef __CUDACC__
+// first_cell_u64 with the 64-bit remainder through the prime's magic
+// m64 = floor(2^64 / p): the quotient estimate umulhi(q_w, m64) is exact or
+// one low, so one correction (instead of a software 64-bit division).
+__device__ __forceinline__ uint64_t first_cell_magic(uint64_t q_w, uint64_t p, uint64_t m64) {
+    const uint64_t pp = p * p;
+    if (pp >= q_w) return (pp - q_w) >> 1;
+    uint64_t r = q_w - __umul64hi(q_w, m64) * p;
+    if (r >= p) r -= p;
+    uint64_t d = r ? p - r : 0;
+    if (d & 1) d += p;
+    return d >> 1;
+}
+#endif
+
 // x mod p for p >= 1024, x < 2^32, via an fp32 reciprocal estimate; the
 // estimate is off by at most 2, fixed by the correction loops.
 __device__ __forceinline__ uint32_t mod_fp(uint32_t x, uint32_t p, float rp) {

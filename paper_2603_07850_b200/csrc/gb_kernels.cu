@@ -307,14 +307,14 @@ __global__ void k_compact(const uint32_t* __restrict__ bits, uint64_t n_words, u
 // multiple of p >= max(p^2, qbase), clamped to 2^31 - 1 (pieces hold fewer
 // cells, so a clamped c0 strikes nothing).  One 16-B load per prime per block.
 __global__ void k_segment_offsets(const SegJob* __restrict__ jobs, uint32_t nslots,
-                                  const uint32_t* __restrict__ primes, uint32_t iA0, uint32_t np,
-                                  uint4* __restrict__ pmc) {
+                                  const uint32_t* __restrict__ primes, const uint64_t* __restrict__ m64,
+                                  uint32_t iA0, uint32_t np, uint4* __restrict__ pmc) {
     uint64_t total = (uint64_t)nslots * np;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
          t += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t s = (uint32_t)(t / np), i = (uint32_t)(t % np);
         const uint32_t p = primes[iA0 + i];
-        const uint64_t c = first_cell_u64(jobs[s].qbase, p);
+        const uint64_t c = first_cell_magic(jobs[s].qbase, p, m64[iA0 + i]);
         const uint32_t c0 = c >= 0x7FFFFFFFull ? 0x7FFFFFFFu : (uint32_t)c;
         pmc[t] = make_uint4(p, (uint32_t)((1ull << 32) / p), p - 1 - c0, c0);
     }
@@ -323,7 +323,8 @@ __global__ void k_segment_offsets(const SegJob* __restrict__ jobs, uint32_t nslo
 // Primes above P_TILE_MAX: strike the slot's global bitmask (cells relative
 // to qbase) with RED.AND; K2 ANDs the words into its tile.
 __global__ void k_large_strike(const SegJob* __restrict__ jobs, uint32_t nslots,
-                               const uint32_t* __restrict__ primes, uint64_t iL0, uint64_t iL1,
+                               const uint32_t* __restrict__ primes, const uint64_t* __restrict__ m64,
+                               uint64_t iL0, uint64_t iL1,
                                uint32_t* __restrict__ qg, uint64_t qg_stride_words) {
     uint64_t np = iL1 - iL0;
     uint64_t total = np * nslots;
@@ -334,7 +335,7 @@ __global__ void k_large_strike(const SegJob* __restrict__ jobs, uint32_t nslots,
         const SegJob& j = jobs[s];
         uint64_t ncells = (uint64_t)j.qg_words * 32;
         uint64_t p = primes[i];
-        uint64_t c = first_cell_u64(j.qbase, p);
+        uint64_t c = first_cell_magic(j.qbase, p, m64[i]);
         uint32_t* g = qg + s * qg_stride_words;
         for (; c < ncells; c += p) atomicAnd(&g[c >> 5], ~(1u << (c & 31)));
     }
@@ -1131,6 +1132,12 @@ __global__ void k_finalize(const SegJob* __restrict__ jobs, uint32_t nslots, con
     }
 }
 
+// m64[i] = floor(2^64 / p_i) (p odd > 1, so = floor((2^64 - 1) / p_i))
+__global__ void k_prime_magic64(const uint32_t* __restrict__ primes, uint64_t n, uint64_t* __restrict__ m64) {
+    for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x)
+        m64[i] = ~0ull / primes[i];
+}
+
 // ============================================================ smem peak
 // Conflict-free 128-bit shared-memory loads from every resident warp: the
 // measured roofline denominator of the fused kernel (128 B/clk/SM nominal).
@@ -1194,20 +1201,26 @@ cudaError_t launch_compact(const uint32_t* bits, uint64_t n_words, uint32_t chun
     k_compact<<<(unsigned)n_chunks, 256, 0, st>>>(bits, n_words, chunk, offsets, lo, primes);
     return cudaGetLastError();
 }
+cudaError_t launch_prime_magic64(const uint32_t* primes, uint64_t n, uint64_t* m64, cudaStream_t st) {
+    if (!n) return cudaSuccess;
+    unsigned grid = (unsigned)std::min<uint64_t>((n + 255) / 256, 148ull * 16);
+    k_prime_magic64<<<grid, 256, 0, st>>>(primes, n, m64);
+    return cudaGetLastError();
+}
 cudaError_t launch_segment_offsets(const SegJob* jobs, uint32_t nslots, const uint32_t* primes,
-                                   uint32_t iA0, uint32_t np, uint4* pmc, cudaStream_t st) {
+                                   const uint64_t* m64, uint32_t iA0, uint32_t np, uint4* pmc, cudaStream_t st) {
     uint64_t total = (uint64_t)nslots * np;
     if (!total) return cudaSuccess;
     unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
-    k_segment_offsets<<<grid, 256, 0, st>>>(jobs, nslots, primes, iA0, np, pmc);
+    k_segment_offsets<<<grid, 256, 0, st>>>(jobs, nslots, primes, m64, iA0, np, pmc);
     return cudaGetLastError();
 }
-cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, uint64_t iL0,
-                                uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, cudaStream_t st) {
+cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, const uint64_t* m64,
+                                uint64_t iL0, uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, cudaStream_t st) {
     uint64_t total = (uint64_t)nslots * (iL1 - iL0);
     if (!total) return cudaSuccess;
     unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 32);
-    k_large_strike<<<grid, 256, 0, st>>>(jobs, nslots, primes, iL0, iL1, qg, qg_stride_words);
+    k_large_strike<<<grid, 256, 0, st>>>(jobs, nslots, primes, m64, iL0, iL1, qg, qg_stride_words);
     return cudaGetLastError();
 }
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st) {

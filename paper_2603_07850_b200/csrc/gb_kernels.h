@@ -68,10 +68,11 @@ cudaError_t launch_scan(const uint32_t* counts, uint64_t n, uint64_t* offsets, u
                         cudaStream_t st);
 cudaError_t launch_compact(const uint32_t* bits, uint64_t n_words, uint32_t chunk, const uint64_t* offsets,
                            uint64_t lo, uint32_t* primes, uint64_t n_chunks, cudaStream_t st);
+cudaError_t launch_prime_magic64(const uint32_t* primes, uint64_t n, uint64_t* m64, cudaStream_t st);
 cudaError_t launch_segment_offsets(const SegJob* jobs, uint32_t nslots, const uint32_t* primes,
-                                   uint32_t iA0, uint32_t np, uint4* pmc, cudaStream_t st);
-cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, uint64_t iL0,
-                                uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, cudaStream_t st);
+                                   const uint64_t* m64, uint32_t iA0, uint32_t np, uint4* pmc, cudaStream_t st);
+cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, const uint64_t* m64,
+                                uint64_t iL0, uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, cudaStream_t st);
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_stragglers(const SegJob* jobs, const StragEntry* list, const unsigned int* list_count,
                               uint32_t list_cap, uint64_t p_small, StragResult* res, uint64_t* pmin_out,
