@@ -101,6 +101,8 @@ struct gb_dev {
     uint64_t iL0 = 0, iL1 = 0;          // large primes
     uint32_t* d_pat = nullptr;
     uint64_t* d_pmr = nullptr;
+    uint32_t* d_pat6 = nullptr;         // wheel-6 presieve patterns
+    uint64_t* d_masks6 = nullptr;       // wheel-6 deep-window masks
     uint64_t max_piece = 0;
     uint64_t qg_stride = 0; // words per slot
     Batch batches[NBATCH];
@@ -183,20 +185,34 @@ static void batch_free(gb_dev* d, Batch& b) {
     b = Batch{};
 }
 
-// Fill the job descriptor of one piece.
+// Fill the job descriptor of one piece: wheel-6 blocks of E6 evens whose
+// windows start at Q_b = Q + 6 K6 b, Q = the largest q = 1 (mod 6) with
+// q <= a - PH6 (negative near the start of the number line).
 static void make_job(gb_dev* d, const Piece& pc, SegJob& j, uint32_t prefix) {
     j.a = pc.a;
     j.b = pc.b;
     j.evens = (uint32_t)(((pc.b - pc.a) >> 1) + 1);
-    j.nblocks = (j.evens + E - 1) / E;
+    j.nblocks = (j.evens + E6 - 1) / E6;
     j.block_prefix = prefix;
-    bool low = (pc.a - 3) < 2ull * JH;
-    j.b1 = low ? 1 : 0;
-    // q of cell 0 of block b1: a - 3 - 2JH + 2*b1*E (>= 3 in both cases)
-    j.qbase = (pc.a - 3 + 2ull * j.b1 * E) - 2ull * JH;
-    uint64_t cells = (uint64_t)j.nblocks * E + JH;
-    j.qg_words = (!low && d->iL1 > d->iL0) ? (uint32_t)((cells + 31) / 32) : 0;
-    j.pad = 0;
+    if (pc.a >= PH6 + 1) {
+        const uint64_t x = pc.a - PH6; // >= 1
+        const uint64_t q = x - ((x - 1) % 6);
+        j.qneg = 0;
+        j.qbase = q;
+        j.delta = (uint32_t)(pc.a - q);
+        for (int g = 0; g < 4; ++g) j.qmod[g] = (uint32_t)(q % pg6_p(g));
+    } else {
+        const int64_t x = (int64_t)pc.a - (int64_t)PH6; // <= 0
+        const int64_t q = x - (((x - 1) % 6) + 6) % 6;
+        j.qneg = 1;
+        j.qbase = (uint64_t)(-q);
+        j.delta = (uint32_t)((int64_t)pc.a - q);
+        for (int g = 0; g < 4; ++g) {
+            const int64_t P = pg6_p(g);
+            j.qmod[g] = (uint32_t)(((q % P) + P) % P);
+        }
+    }
+    j.qg_words = d->iL1 > d->iL0 ? (uint32_t)(((uint64_t)j.nblocks * K6 + (M6 - K6) + 31) / 32) : 0;
 }
 
 static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
@@ -232,6 +248,8 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     A.nslots = n;
     A.total_blocks = prefix;
     A.primes = d->d_primes;
+    A.n_primes = d->n_primes;
+    A.sbound = std::max<uint64_t>(d->sqrt_bound, 47);
     A.iA0 = d->iA0;
     A.iA1 = d->iA1;
     A.iB1 = d->iB1;
@@ -241,8 +259,8 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     A.wsplit = d->d_wsplit;
     A.qg = large ? b.d_qg : nullptr;
     A.qg_stride_words = d->qg_stride;
-    A.gpat = d->d_pat;
-    A.pmr = d->d_pmr;
+    A.gpat6 = d->d_pat6;
+    A.masks6 = d->d_masks6;
     A.p_small = d->prm.p_small;
     A.inject = d->prm.inject_fail;
     A.block_counter = b.d_counters;
@@ -481,7 +499,9 @@ static int device_odd_primes_upto(gb_dev* d, uint64_t L, uint32_t** d_out, uint6
 static int build_tables(gb_dev* d) {
     CU(d, dmalloc(d->device, &d->d_pat, PAT_WORDS * 4));
     CU(d, dmalloc(d->device, &d->d_pmr, NWIN * 8));
-    CU(d, launch_init_tables(d->d_pat, d->d_pmr, d->prm.p_small, d->sync.st));
+    CU(d, dmalloc(d->device, &d->d_pat6, PAT6_WORDS * 4));
+    CU(d, dmalloc(d->device, &d->d_masks6, 3 * NWIN6 * 8));
+    CU(d, launch_init_tables(d->d_pat, d->d_pmr, d->d_pat6, d->d_masks6, d->prm.p_small, d->sync.st));
     d->launches++;
     int rc = device_odd_primes_upto(d, d->sqrt_bound, &d->d_primes, &d->n_primes);
     if (rc) return rc;
@@ -493,7 +513,7 @@ static int build_tables(gb_dev* d) {
     d->iA0 = (uint32_t)(std::lower_bound(hp.begin(), hp.end(), FIRST_STRIKE_P) - hp.begin());
     d->iA1 = (uint32_t)(std::lower_bound(hp.begin(), hp.end(), P_WARP_MAX) - hp.begin());
     d->iB1 = (uint32_t)(std::upper_bound(hp.begin(), hp.end(), P_TILE_MAX) - hp.begin());
-    d->iW1 = std::max(d->iA1, std::min(d->iB1, (uint32_t)(std::lower_bound(hp.begin(), hp.end(), W) - hp.begin())));
+    d->iW1 = std::max(d->iA1, std::min(d->iB1, (uint32_t)(std::lower_bound(hp.begin(), hp.end(), M6) - hp.begin())));
     d->iL0 = d->iB1;
     d->iL1 = total;
     {
@@ -508,7 +528,7 @@ static int build_tables(gb_dev* d) {
                 if (cnt[w] < 32 && (best < 0 || load[w] < load[best])) best = w;
             if (best < 0) GB_FAIL(d, GB_ERR_INTERNAL, "too many warp-cooperative primes");
             ws[best * 32 + cnt[best]++] = (uint16_t)(i - d->iA0);
-            load[best] += (double)W / (32.0 * hp[i]) + 4.0;
+            load[best] += 2.0 * M6 / (32.0 * hp[i]) + 6.0;
         }
         CU(d, dmalloc(d->device, &d->d_wsplit, ws.size() * sizeof(uint16_t)));
         CU(d, cudaMemcpy(d->d_wsplit, ws.data(), ws.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
@@ -587,8 +607,8 @@ int gb_open(int device, const gb_params* params, gb_dev** out) {
         if ((rc = build_tables(d)) != GB_OK) break;
         const double t_open2 = now_s();
         d->max_piece = std::min<uint64_t>(d->prm.max_seg_evens, MAX_PIECE);
-        uint64_t blocks = (d->max_piece + E - 1) / E;
-        d->qg_stride = (blocks * E + JH + 31) / 32;
+        uint64_t blocks = (d->max_piece + E6 - 1) / E6;
+        d->qg_stride = 2 * ((blocks * K6 + (M6 - K6) + 31) / 32); // arrays A and B
         if ((rc = batch_alloc(d, d->sync, true)) != GB_OK) break;
         for (int i = 0; i < NBATCH && rc == GB_OK; ++i) rc = batch_alloc(d, d->batches[i], true);
         if (getenv("GB_DEBUG_OPEN"))
@@ -617,6 +637,8 @@ int gb_close(gb_dev* d) {
     dfree(d->device, d->flush_buf);
     dfree(d->device, d->d_pat);
     dfree(d->device, d->d_pmr);
+    dfree(d->device, d->d_pat6);
+    dfree(d->device, d->d_masks6);
     dfree(d->device, d->d_wsplit);
     dfree(d->device, d->d_m64);
     delete d;
@@ -817,7 +839,7 @@ uint64_t gb_estimate_device_bytes(uint64_t cover_limit, uint64_t p_small, uint64
     const uint64_t np_all = pi_upper(s);
     const uint64_t np_tile = std::min<uint64_t>(np_all, pi_upper(P_TILE_MAX));
     const uint64_t piece = std::min<uint64_t>(max_seg_evens, MAX_PIECE);
-    const uint64_t qg = s > P_TILE_MAX ? SLOTS * (((piece + E - 1) / E) * E + JH + 31) / 32 * 4 : 0;
+    const uint64_t qg = s > P_TILE_MAX ? SLOTS * 2 * ((((piece + E6 - 1) / E6) * K6 + (M6 - K6) + 31) / 32) * 4 : 0;
     const uint64_t per_batch = SLOTS * np_tile * sizeof(uint4) + qg + (uint64_t)LIST_CAP * (sizeof(StragEntry) + sizeof(StragResult)) +
                                SLOTS * (sizeof(SegJob) + sizeof(SlotAcc) + sizeof(DevRecord)) + 64;
     // base primes + their 64-bit magics + K1 scratch bitmap (transient) + NBATCH + 1 batches
@@ -838,6 +860,16 @@ int gb_device_memory(int device, uint64_t* free_bytes, uint64_t* total_bytes) {
     *free_bytes = fr;
     *total_bytes = tot;
     return GB_OK;
+}
+
+// Debug counters of a GB_STATS build (tools/variants.sh); GB_ERR_PARAM in
+// regular builds.  Not part of the reference interface.
+extern "C" int gb_debug_stats(uint64_t* out8, int reset) {
+    if (!out8) return GB_ERR_PARAM;
+    unsigned long long v[8];
+    const int rc = debug_stats(v, reset);
+    for (int i = 0; i < 8; ++i) out8[i] = v[i];
+    return rc == 0 ? GB_OK : GB_ERR_PARAM;
 }
 
 int gb_launch_count(const gb_dev* d, uint64_t* launches) {

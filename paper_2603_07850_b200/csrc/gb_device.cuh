@@ -30,17 +30,14 @@ constexpr int CTAS_PER_SM = W_LOG2 >= 20 ? 1 : 2;
 constexpr int NWARPS = THREADS / 32;
 // Warp-specialised fused kernel (k_verify_ws): one CTA of WS_THREADS per SM,
 // WS_ST sieve threads + WS_CT check threads.
-#ifndef GB_WS
-#define GB_WS 1
-#endif
 #ifndef GB_WS_SIEVE_WARPS
-#define GB_WS_SIEVE_WARPS 16
+#define GB_WS_SIEVE_WARPS 12
 #endif
 constexpr int WS_THREADS = 1024;
 constexpr int WS_ST = 32 * GB_WS_SIEVE_WARPS;
 constexpr int WS_CT = WS_THREADS - WS_ST;
 // warps of the group that runs the warp-cooperative strikes
-constexpr int SPLIT_WARPS = GB_WS ? WS_ST / 32 : NWARPS;
+constexpr int SPLIT_WARPS = WS_ST / 32;
 constexpr uint32_t P_TILE_MAX = 1u << 22; // base primes above: K_large (global strikes)
 constexpr uint32_t P_WARP_MAX = 1024;     // primes below: warp-cooperative strikes
 constexpr uint32_t FIRST_STRIKE_P = 53;   // primes below are in the presieve patterns
@@ -66,6 +63,41 @@ __host__ __device__ constexpr uint32_t pat_prime(int t) {
 }
 constexpr int N_PAT_PRIMES = 14;
 
+// ---------------------------------------------------------------- wheel-6
+// The fused kernel sieves a wheel-6 tile: array A holds q = Q + 6k
+// (q = 1 mod 6), array B holds q = Q + 4 + 6k (q = 5 mod 6), k < M6; Q = 1
+// (mod 6) is the block's window origin.  Multiples of 2 and 3 have no cell,
+// so a 64 KiB tile spans 6 M6 = 1.57 M integers (odd-only: 1.05 M) and an
+// even n meets only the candidates p with n - p = +-1 (mod 6).  Blocks of a
+// slot advance by K6 cells (a multiple of 32, so global bitmask words align)
+// and hold E6 = 3 K6 evens; consecutive windows overlap by 6 (M6 - K6) > PH6
+// integers, the Phase 1 halo.
+constexpr uint32_t M6 = 1u << 18;             // cells per class array
+constexpr uint32_t M6W = M6 / 32;             // words per class array
+constexpr uint32_t K6 = 260768;               // block stride in cells (32 * 8149)
+constexpr uint32_t E6 = 3 * K6;               // evens per block (782304)
+constexpr uint32_t PH6 = 8193;                // in-tile candidates p <= PH6
+constexpr int NWIN6 = 22;                     // 64-wide g-windows, g = p div 6 <= 1365
+constexpr uint32_t TPAD = 4;                  // zero words before / after each array (16-B aligned)
+constexpr uint32_t TILE6_WORDS = 3 * TPAD + 2 * M6W; // [pad][A][pad][B][pad]
+static_assert(K6 % 32 == 0 && 6 * (M6 - K6) > PH6 + 5, "wheel-6 block geometry");
+static_assert(64 * NWIN6 * 6 >= PH6, "deep windows cover the halo");
+
+// wheel-6 presieve groups: pattern bit k is 0 iff a prime of the group
+// divides 6k + 1 (3 has no cells)
+__host__ __device__ constexpr uint32_t pg6_p(int g) {
+    return g == 0 ? 5005u : g == 1 ? 7429u : g == 2 ? 33263u : 82861u; // 5·7·11·13, 17·19·23, 29·31·37, 41·43·47
+}
+__host__ __device__ constexpr uint32_t pg6_off(int g) {
+    return (g > 0 ? pat_words(pg6_p(0)) : 0u) + (g > 1 ? pat_words(pg6_p(1)) : 0u) +
+           (g > 2 ? pat_words(pg6_p(2)) : 0u) + (g > 3 ? pat_words(pg6_p(3)) : 0u);
+}
+constexpr uint32_t PAT6_WORDS = pg6_off(4);
+// 6^-1 mod x for x coprime to 6
+__host__ __device__ constexpr uint32_t inv6_mod(uint32_t x) {
+    return x % 6 == 1 ? (uint32_t)((5ull * x + 1) / 6) : (uint32_t)((x + 1) / 6);
+}
+
 // straggler list entry flags
 constexpr uint32_t F_NEED_P1 = 1u;      // continue Phase 1 from j_next
 constexpr uint32_t F_P1_FAIL = 2u;      // Phase 1 exhausted: unverified
@@ -84,16 +116,20 @@ struct StragResult {
     uint64_t p2;      // Phase 2 minimal p (0 = none / not run)
 };
 
-// Device-side per-segment job (one per batch slot).
+// Device-side per-segment job (one per batch slot).  Block b of the slot
+// has window origin Q_b = Q + 6 K6 b and evens a + 2 E6 b ...; Q = the
+// largest q = 1 (mod 6) with q <= a - PH6, possibly negative near the start
+// of the number line (then qneg = 1 and qbase = -Q).
 struct SegJob {
     uint64_t a, b;          // evens [a, b]
-    uint64_t qbase;         // q of cell 0 of block b1 (see b1)
+    uint64_t qbase;         // |Q|
     uint32_t evens;         // (b - a)/2 + 1  (<= MAX_SEG_EVENS)
-    uint32_t nblocks;       // ceil(evens / E)
+    uint32_t nblocks;       // ceil(evens / E6)
     uint32_t block_prefix;  // flat index of this slot's first block
-    uint32_t b1;            // 1 if block 0 is the low block (window at q = 1)
-    uint32_t qg_words;      // words of the large-prime bitmask (0 = none)
-    uint32_t pad;
+    uint32_t qneg;          // Q = -qbase
+    uint32_t qg_words;      // words per class array of the large-prime bitmask (0 = none)
+    uint32_t delta;         // a - Q (in [PH6, PH6 + 5])
+    uint32_t qmod[4];       // Q mod pg6_p(g) (non-negative)
 };
 
 // Per-slot accumulator written by the kernels.

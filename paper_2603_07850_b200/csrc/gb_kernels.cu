@@ -25,9 +25,29 @@
 
 namespace gbk {
 
+#ifdef GB_STATS
+// debug counters (variant builds only): 0 generic evens, 1 in-place deep
+// evens (queue overflow), 2 queued deep evens, 3 deep rounds, 4 stragglers,
+// 5 fast blocks, 6 generic blocks
+__device__ unsigned long long g_stats[8];
+#define GB_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
+#else
+#define GB_STAT(i, v) ((void)0)
+#endif
+
 // ============================================================ table init
-// Presieve patterns and the reversed Phase 1 prime masks.
-__global__ void k_init_tables(uint32_t* pat, uint64_t* pmr, uint64_t p_small) {
+// Presieve patterns (odd-only for K1, wheel-6 for the fused kernel), the
+// reversed Phase 1 prime masks of K1's parity hook, and the wheel-6 deep
+// masks: masks6[c * NWIN6 + j] bit 63 - m set iff p = 6 g + off_c (g = 64 j
+// + m; off = +1, -1, +5 for c = 0, 1, 2) is prime, 5 <= p <= min(p_small, PH6).
+__device__ bool small_prime(uint32_t p) {
+    if (p < 2) return false;
+    for (uint32_t d = 2; d * d <= p; ++d)
+        if (p % d == 0) return false;
+    return true;
+}
+
+__global__ void k_init_tables(uint32_t* pat, uint64_t* pmr, uint32_t* pat6, uint64_t* masks6, uint64_t p_small) {
     const uint32_t gp[4][3] = {{3, 5, 7}, {17, 19, 23}, {29, 31, 37}, {41, 43, 47}};
     const uint32_t gp1x[2] = {11, 13};
     uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -47,6 +67,20 @@ __global__ void k_init_tables(uint32_t* pat, uint64_t* pmr, uint64_t p_small) {
             }
             pat[pg_off(g) + w] = v;
         }
+        // wheel-6: bit k <-> 6k + 1 (mod P); group 0 is 5·7·11·13
+        const uint32_t P6 = pg6_p(g);
+        const uint32_t nw6 = pg6_off(g + 1) - pg6_off(g);
+        for (uint32_t w = tid; w < nw6; w += nthr) {
+            uint32_t v = 0;
+            for (int bit = 0; bit < 32; ++bit) {
+                const uint64_t val = 6ull * ((w * 32 + bit) % P6) + 1;
+                bool comp = false;
+                if (g == 0) comp = val % 5 == 0 || val % 7 == 0 || val % 11 == 0 || val % 13 == 0;
+                else for (int t = 0; t < 3; ++t) comp |= (val % gp[g][t]) == 0;
+                if (!comp) v |= 1u << bit;
+            }
+            pat6[pg6_off(g) + w] = v;
+        }
     }
     // pmr[k] bit (63 - j') set iff p = 3 + 2(64k + j') is prime and <= p_small
     for (uint32_t k = tid; k < (uint32_t)NWIN; k += nthr) {
@@ -58,6 +92,17 @@ __global__ void k_init_tables(uint32_t* pat, uint64_t* pmr, uint64_t p_small) {
             if (pr) m |= 1ull << (63 - jp);
         }
         pmr[k] = m;
+    }
+    const uint64_t pmax = p_small < PH6 ? p_small : PH6;
+    for (uint32_t e = tid; e < 3u * NWIN6; e += nthr) {
+        const uint32_t cls = e / NWIN6, j = e % NWIN6;
+        const int off = cls == 0 ? 1 : cls == 1 ? -1 : 5;
+        uint64_t m = 0;
+        for (int jm = 0; jm < 64; ++jm) {
+            const int64_t p = 6 * (int64_t)(64 * j + jm) + off;
+            if (p >= 5 && (uint64_t)p <= pmax && small_prime((uint32_t)p)) m |= 1ull << (63 - jm);
+        }
+        masks6[e] = m;
     }
 }
 
@@ -302,10 +347,24 @@ __global__ void k_compact(const uint32_t* __restrict__ bits, uint64_t n_words, u
 }
 
 // ============================================================ segment setup
-// pmc[s*np + i] = {p, floor(2^32/p), p - 1 - c0, c0} of tile prime i (index
-// iA0 + i): c0 = cell (relative to the slot's qbase) of the first odd
-// multiple of p >= max(p^2, qbase), clamped to 2^31 - 1 (pieces hold fewer
-// cells, so a clamped c0 strikes nothing).  One 16-B load per prime per block.
+// x mod p through the prime's 64-bit magic (quotient estimate exact or one low)
+__device__ __forceinline__ uint64_t mod_magic(uint64_t x, uint64_t p, uint64_t m64) {
+    const uint64_t r = x - __umul64hi(x, m64) * p;
+    return r >= p ? r - p : r;
+}
+
+// First index k >= 0 of array A (q = Q + 6k) with p | q: (-Q) 6^-1 mod p.
+__device__ __forceinline__ uint32_t first_a6(const SegJob& J, uint32_t p, uint64_t m64) {
+    uint64_t r = mod_magic(J.qbase, p, m64); // |Q| mod p
+    if (!J.qneg) r = r ? p - r : 0;          // (-Q) mod p
+    return (uint32_t)mod_magic(r * inv6_mod(p), p, m64);
+}
+
+// pmc[s*np + i] = {p, floor(2^32/p), p - 1 - k0, 4 6^-1 mod p} of tile prime
+// i (index iA0 + i), k0 = first_a6 at the slot's window origin; array B's
+// first index is k0 - 4 6^-1 (mod p).  Strikes start at the first multiple in
+// the window, not at p^2: multiples below p^2 are composite anyway, and q = p
+// itself is restored by the low-window fix-up (fixup_low6).
 __global__ void k_segment_offsets(const SegJob* __restrict__ jobs, uint32_t nslots,
                                   const uint32_t* __restrict__ primes, const uint64_t* __restrict__ m64,
                                   uint32_t iA0, uint32_t np, uint4* __restrict__ pmc) {
@@ -314,18 +373,17 @@ __global__ void k_segment_offsets(const SegJob* __restrict__ jobs, uint32_t nslo
          t += (uint64_t)gridDim.x * blockDim.x) {
         uint32_t s = (uint32_t)(t / np), i = (uint32_t)(t % np);
         const uint32_t p = primes[iA0 + i];
-        const uint64_t c = first_cell_magic(jobs[s].qbase, p, m64[iA0 + i]);
-        const uint32_t c0 = c >= 0x7FFFFFFFull ? 0x7FFFFFFFu : (uint32_t)c;
-        pmc[t] = make_uint4(p, (uint32_t)((1ull << 32) / p), p - 1 - c0, c0);
+        const uint32_t k0 = first_a6(jobs[s], p, m64[iA0 + i]);
+        pmc[t] = make_uint4(p, (uint32_t)((1ull << 32) / p), p - 1 - k0, (uint32_t)((4ull * inv6_mod(p)) % p));
     }
 }
 
-// Primes above P_TILE_MAX: strike the slot's global bitmask (cells relative
-// to qbase) with RED.AND; K2 ANDs the words into its tile.
+// Primes above P_TILE_MAX: strike the slot's global wheel-6 bitmask (array A
+// then array B, qg_words words each, cells relative to the slot's origin)
+// with RED.AND; the fused kernel ANDs the words into its tiles.
 __global__ void k_large_strike(const SegJob* __restrict__ jobs, uint32_t nslots,
                                const uint32_t* __restrict__ primes, const uint64_t* __restrict__ m64,
-                               uint64_t iL0, uint64_t iL1,
-                               uint32_t* __restrict__ qg, uint64_t qg_stride_words) {
+                               uint64_t iL0, uint64_t iL1, uint32_t* __restrict__ qg, uint64_t qg_stride_words) {
     uint64_t np = iL1 - iL0;
     uint64_t total = np * nslots;
     for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
@@ -333,109 +391,117 @@ __global__ void k_large_strike(const SegJob* __restrict__ jobs, uint32_t nslots,
         uint32_t s = (uint32_t)(t / np);
         uint64_t i = iL0 + t % np;
         const SegJob& j = jobs[s];
-        uint64_t ncells = (uint64_t)j.qg_words * 32;
-        uint64_t p = primes[i];
-        uint64_t c = first_cell_magic(j.qbase, p, m64[i]);
-        uint32_t* g = qg + s * qg_stride_words;
-        for (; c < ncells; c += p) atomicAnd(&g[c >> 5], ~(1u << (c & 31)));
+        const uint64_t ncells = (uint64_t)j.qg_words * 32;
+        const uint32_t p = primes[i];
+        const uint32_t k0 = first_a6(j, p, m64[i]);
+        const uint32_t c = (uint32_t)((4ull * inv6_mod(p)) % p);
+        const uint32_t k0b = k0 >= c ? k0 - c : k0 + p - c;
+        uint32_t* ga = qg + s * qg_stride_words;
+        uint32_t* gb = ga + j.qg_words;
+        for (uint64_t k = k0; k < ncells; k += p) atomicAnd(&ga[k >> 5], ~(1u << (k & 31)));
+        for (uint64_t k = k0b; k < ncells; k += p) atomicAnd(&gb[k >> 5], ~(1u << (k & 31)));
     }
 }
 
 // ============================================================ K2 + K3
-// Window cell of the first strike of {p, m, d = p - 1 - c0, c0} in the block
-// starting at cell B (relative to qbase); >= W means no strike.
-//   c0 >= B: c0 - B.   c0 < B: (c0 - B) mod p = p - 1 - ((B + d) mod p).
-// The mod is exact through the magic m = floor(2^32/p) (quotient low by at
-// most one).  When c0 - B >= p, B + d wraps and the mod term is some value
-// < p <= c0 - B, so a signed max selects the right case without a branch.
-__device__ __forceinline__ uint32_t block_off(const uint4 v, uint32_t B) {
+// Wheel-6 tile: [TPAD][A: M6W words][TPAD][B: M6W words][TPAD], pads zero.
+__device__ __forceinline__ uint32_t* arr_a(uint32_t* t) { return t + TPAD; }
+__device__ __forceinline__ uint32_t* arr_b(uint32_t* t) { return t + 2 * TPAD + M6W; }
+__device__ __forceinline__ const uint32_t* arr_a(const uint32_t* t) { return t + TPAD; }
+__device__ __forceinline__ const uint32_t* arr_b(const uint32_t* t) { return t + 2 * TPAD + M6W; }
+
+// Window cells of the first strikes of {p, m, d = p - 1 - k0, c} in arrays A
+// and B of the block starting at cell KB: (k0 - KB) mod p = p - 1 - ((KB + d)
+// mod p) by the magic m = floor(2^32/p) (quotient low by at most one), and
+// B's = A's - c (mod p).  Branch-free.
+__device__ __forceinline__ void block_off6(const uint4 v, uint32_t KB, uint32_t& oa, uint32_t& ob) {
     const uint32_t p = v.x;
-    const uint32_t y = B + v.z;
+    const uint32_t y = KB + v.z;
     uint32_t r = y - __umulhi(y, v.y) * p;
     r = min(r, r - p);
-    const int32_t o_mod = (int32_t)(p - 1 - r);
-    const int32_t o_dir = (int32_t)(v.w - B);
-    return (uint32_t)max(o_dir, o_mod);
+    oa = p - 1 - r;
+    const uint32_t t = oa - v.w;
+    ob = oa >= v.w ? t : t + p;
 }
 
-// low window (q_w = 1): first strike at p^2
-__device__ __forceinline__ uint32_t low_off(uint32_t p) {
-    const uint64_t c = ((uint64_t)p * p - 1) >> 1;
-    return c < W ? (uint32_t)c : W;
-}
-
-// Warp-cooperative strikes of one prime from window cell o: lane L strikes
-// o + L p + k 32p.  32p cells are p words, so the lane's bit (and mask) is
-// fixed and only the word index advances.
-__device__ __forceinline__ void strike_warp(uint32_t* tile, uint32_t o, uint32_t p, uint32_t lane) {
+// Warp-cooperative strikes of one prime in one class array from cell o:
+// lane L strikes o + L p + k 32p; 32p cells are p words, so the lane's mask
+// is loop-invariant and only the word index advances.
+__device__ __forceinline__ void strike_warp6(uint32_t* arr, uint32_t o, uint32_t p, uint32_t lane) {
     const uint32_t c = o + lane * p;
-    if (c >= W) return;
+    if (c >= M6) return;
     const uint32_t mask = __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, c);
     uint32_t wi = c >> 5;
     const uint32_t p2 = 2 * p, p3 = 3 * p, p4 = 4 * p;
-    for (; wi + p3 < (uint32_t)TILE_WORDS; wi += p4) {
-        atomicAnd(&tile[wi], mask);
-        atomicAnd(&tile[wi + p], mask);
-        atomicAnd(&tile[wi + p2], mask);
-        atomicAnd(&tile[wi + p3], mask);
+    for (; wi + p3 < M6W; wi += p4) {
+        atomicAnd(&arr[wi], mask);
+        atomicAnd(&arr[wi + p], mask);
+        atomicAnd(&arr[wi + p2], mask);
+        atomicAnd(&arr[wi + p3], mask);
     }
-    for (; wi < (uint32_t)TILE_WORDS; wi += p) atomicAnd(&tile[wi], mask);
+    for (; wi < M6W; wi += p) atomicAnd(&arr[wi], mask);
 }
 
-// K2 strikes of one verify block by a group of GT threads (tid = the
-// thread's index in the group): warp-cooperative below P_WARP_MAX, one
-// thread per prime above; primes >= W (index >= nW) strike at most once.
-// pmc: this slot's {p, m, d, c0} row (index i - iA0).
-template <int GT>
-__device__ __forceinline__ void strike_verify(uint32_t* tile, const uint4* __restrict__ pmc, uint32_t nA,
-                                              uint32_t nW, uint32_t nB, uint32_t B, bool low, uint32_t tid,
-                                              const uint16_t* __restrict__ wsplit) {
-    const uint32_t lane = tid & 31, warp = tid >> 5;
-    if (low) {
-        for (uint32_t i = warp; i < nA; i += GT / 32) {
-            const uint32_t p = __ldg(&pmc[i].x);
-            const uint32_t o = low_off(p);
-            if (o < W) strike_warp(tile, o, p, lane);
-        }
-        for (uint32_t i = nA + tid; i < nB; i += GT) {
-            const uint32_t p = __ldg(&pmc[i].x);
-            strike_run(tile, low_off(p), p);
-        }
-        return;
+// strikes c, c + step, ... < M6 of one class array (two per trip)
+__device__ __forceinline__ void strike_run6(uint32_t* arr, uint32_t c, uint32_t step) {
+    while (c + step < M6) {
+        strike(arr, c);
+        strike(arr, c + step);
+        c += 2 * step;
     }
+    if (c < M6) strike(arr, c);
+}
+
+// K2 strikes of one block by a group of GT threads (tid = index in the
+// group): warp-cooperative below P_WARP_MAX (rows wsplit[warp][..], balanced
+// by the host), one thread per prime above; primes >= M6 (index >= nW)
+// strike each array at most once.  pmc: this slot's rows (index i - iA0).
+template <int GT>
+__device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __restrict__ pmc, uint32_t nA,
+                                               uint32_t nW, uint32_t nB, uint32_t KB, uint32_t tid,
+                                               const uint16_t* __restrict__ wsplit) {
+    const uint32_t lane = tid & 31, warp = tid >> 5;
+    uint32_t* A6 = arr_a(tile);
+    uint32_t* B6 = arr_b(tile);
     {
-        // warp-cooperative primes: warp w takes the rows wsplit[w][0..] (the
-        // host balances sum W/p over warps, longest first); the lanes load
-        // the rows and compute the offsets in parallel, then stride in turn
         const uint32_t idx = wsplit[warp * 32 + lane];
         const uint32_t nmine = __popc(__ballot_sync(0xffffffffu, idx != 0xFFFFu)); // packed from lane 0
-        uint32_t pm = 0, om = W;
+        uint32_t pm = 0, oam = M6, obm = M6;
         if (idx != 0xFFFFu) {
             const uint4 v = __ldg(pmc + idx);
             pm = v.x;
-            om = block_off(v, B);
+            block_off6(v, KB, oam, obm);
         }
         for (uint32_t k = 0; k < nmine; ++k) {
-            const uint32_t o = __shfl_sync(0xffffffffu, om, k);
+            const uint32_t oa = __shfl_sync(0xffffffffu, oam, k);
+            const uint32_t ob = __shfl_sync(0xffffffffu, obm, k);
             const uint32_t p = __shfl_sync(0xffffffffu, pm, k);
-            if (o < W) strike_warp(tile, o, p, lane);
+            strike_warp6(A6, oa, p, lane);
+            strike_warp6(B6, ob, p, lane);
         }
     }
-    // thread per prime; the {p, m, d, c0} rows come from L2, so 4 (8) loads
-    // are issued before their strikes to keep several in flight per warp
+    // thread per prime; the rows come from L2, so 4 (8) loads are issued
+    // before their strikes to keep several in flight per warp
     const uint4* q = pmc + nA + tid;
     const uint4* qe = pmc + nW;
     for (; q + 3 * GT < qe; q += 4 * GT) {
-        const uint4 v0 = __ldg(q), v1 = __ldg(q + GT), v2 = __ldg(q + 2 * GT),
-                    v3 = __ldg(q + 3 * GT);
-        strike_run(tile, block_off(v0, B), v0.x);
-        strike_run(tile, block_off(v1, B), v1.x);
-        strike_run(tile, block_off(v2, B), v2.x);
-        strike_run(tile, block_off(v3, B), v3.x);
+        uint4 v[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u) v[u] = __ldg(q + u * GT);
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            uint32_t oa, ob;
+            block_off6(v[u], KB, oa, ob);
+            strike_run6(A6, oa, v[u].x);
+            strike_run6(B6, ob, v[u].x);
+        }
     }
     for (; q < qe; q += GT) {
         const uint4 v = __ldg(q);
-        strike_run(tile, block_off(v, B), v.x);
+        uint32_t oa, ob;
+        block_off6(v, KB, oa, ob);
+        strike_run6(A6, oa, v.x);
+        strike_run6(B6, ob, v.x);
     }
     q = pmc + nW + tid;
     qe = pmc + nB;
@@ -445,40 +511,108 @@ __device__ __forceinline__ void strike_verify(uint32_t* tile, const uint4* __res
         for (int u = 0; u < 8; ++u) v[u] = __ldg(q + u * GT);
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
-            const uint32_t o = block_off(v[u], B);
-            if (o < W) strike(tile, o);
+            uint32_t oa, ob;
+            block_off6(v[u], KB, oa, ob);
+            if (oa < M6) strike(A6, oa);
+            if (ob < M6) strike(B6, ob);
         }
     }
     for (; q < qe; q += GT) {
         const uint4 v = __ldg(q);
-        const uint32_t o = block_off(v, B);
-        if (o < W) strike(tile, o);
+        uint32_t oa, ob;
+        block_off6(v, KB, oa, ob);
+        if (oa < M6) strike(A6, oa);
+        if (ob < M6) strike(B6, ob);
     }
 }
 
-__device__ __forceinline__ uint64_t window_bits(const uint32_t* tile, int64_t x) {
-    // 64 cells [x-64, x) as a u64 (bit 63 <-> cell x-1); cells < 0 read as 0
-    if (x >= 64) {
-        uint32_t lo = (uint32_t)(x - 64);
-        uint32_t wi = lo >> 5, s = lo & 31;
-        uint32_t w0 = tile[wi], w1 = tile[wi + 1], w2 = tile[wi + 2];
-        uint32_t l32 = __funnelshift_r(w0, w1, s);
-        uint32_t h32 = __funnelshift_r(w1, w2, s);
-        return ((uint64_t)h32 << 32) | l32;
+// Presieve one class array (M6W words) with the wheel-6 patterns; ph[g] =
+// pattern index of the array's cell 0.  Each thread builds 4 consecutive
+// words per step (one 16-B store): per group 5 loads, 4 funnel shifts.
+__device__ __forceinline__ void presieve6(uint32_t* arr, const uint32_t* pat6, const uint32_t (&ph)[4], uint32_t tid,
+                                          uint32_t nthr) {
+    uint32_t o[4], step[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        o[g] = (ph[g] + 128u * tid) % pg6_p(g);
+        step[g] = (128u * nthr) % pg6_p(g);
     }
-    if (x <= 0) return 0;
-    uint64_t v = ((uint64_t)tile[1] << 32) | tile[0];
-    return v << (64 - x);
+    for (uint32_t wd = 4 * tid; wd < M6W; wd += 4 * nthr) {
+        uint4 v = make_uint4(~0u, ~0u, ~0u, ~0u);
+#pragma unroll
+        for (int g = 0; g < 4; ++g) {
+            const uint32_t* pg = pat6 + pg6_off(g) + (o[g] >> 5);
+            const uint32_t sh = o[g];
+            const uint32_t w0 = pg[0], w1 = pg[1], w2 = pg[2], w3 = pg[3], w4 = pg[4];
+            v.x &= __funnelshift_r(w0, w1, sh);
+            v.y &= __funnelshift_r(w1, w2, sh);
+            v.z &= __funnelshift_r(w2, w3, sh);
+            v.w &= __funnelshift_r(w3, w4, sh);
+            const uint32_t on = o[g] + step[g];
+            o[g] = min(on, on - pg6_p(g));
+        }
+        *reinterpret_cast<uint4*>(arr + wd) = v;
+    }
 }
 
-// ------------------------------------------------------------ K3 helpers
-// 64 cells [x-64, x) as a u64 (bit 63 <-> cell x-1), x >= 64.
-__device__ __forceinline__ uint64_t window_bits_hi(const uint32_t* tile, uint32_t x) {
-    const uint32_t lo = x - 64;
-    const uint32_t wi = lo >> 5, sh = lo & 31;
-    const uint32_t w0 = tile[wi], w1 = tile[wi + 1], w2 = tile[wi + 2];
+__device__ __forceinline__ void set_cell(uint32_t* arr, uint32_t k) { atomicOr(&arr[k >> 5], 1u << (k & 31)); }
+__device__ __forceinline__ void clear_cell(uint32_t* arr, uint32_t k) { atomicAnd(&arr[k >> 5], ~(1u << (k & 31))); }
+
+// Window of a block whose origin Qs (signed) is at most sbound: q <= 1 is
+// not prime, and every base prime p >= 5 inside the window (struck as a
+// multiple of itself, or presieved) is restored.
+__device__ __forceinline__ void fixup_low6(uint32_t* tile, int64_t Qs, const uint32_t* __restrict__ primes,
+                                           uint64_t n_primes, uint64_t sbound, uint32_t tid, uint32_t nthr) {
+    uint32_t* A6 = arr_a(tile);
+    uint32_t* B6 = arr_b(tile);
+    // cells with q <= 1 (A: Qs + 6k <= 1, B: Qs + 4 + 6k <= 1)
+    if (Qs <= 1) {
+        const int64_t na6 = (1 - Qs) / 6 + 1;
+        const uint32_t na = na6 < (int64_t)M6 ? (uint32_t)na6 : M6;
+        for (uint32_t k = tid; k < na; k += nthr) clear_cell(A6, k);
+    }
+    if (Qs <= -3) {
+        const int64_t nb6 = (-3 - Qs) / 6 + 1;
+        const uint32_t nb = nb6 < (int64_t)M6 ? (uint32_t)nb6 : M6;
+        for (uint32_t k = tid; k < nb; k += nthr) clear_cell(B6, k);
+    }
+    // presieved primes 5..47 (their patterns clear them)
+    if (tid < N_PAT_PRIMES - 1) {
+        const int64_t d = (int64_t)pat_prime(tid + 1) - Qs;
+        if (d >= 0 && d < 6 * (int64_t)M6) {
+            if (d % 6 == 0) set_cell(A6, (uint32_t)(d / 6));
+            else set_cell(B6, (uint32_t)((d - 4) / 6));
+        }
+    }
+    // base primes in [max(Qs, 5), min(Qs + 6 M6 - 1, sbound)]
+    const int64_t lo = Qs > 5 ? Qs : 5;
+    const int64_t wend = Qs + 6 * (int64_t)M6 - 1;
+    const int64_t hi = wend < (int64_t)sbound ? wend : (int64_t)sbound;
+    if (lo > hi) return;
+    uint64_t a = 0, b = n_primes; // first index with primes[i] >= lo
+    while (a < b) {
+        const uint64_t m = (a + b) >> 1;
+        if ((int64_t)primes[m] < lo) a = m + 1; else b = m;
+    }
+    for (uint64_t i = a + tid; i < n_primes; i += nthr) {
+        const int64_t p = primes[i];
+        if (p > hi) break;
+        const int64_t d = p - Qs;
+        if (d % 6 == 0) set_cell(A6, (uint32_t)(d / 6));
+        else set_cell(B6, (uint32_t)((d - 4) / 6));
+    }
+}
+
+// 64 cells [x - 64, x) of a class array as a u64 (bit 63 <-> cell x - 1);
+// x may be as low as 64 - 32 TPAD (the leading pad reads as zeros).
+__device__ __forceinline__ uint64_t window6(const uint32_t* arr, int32_t x) {
+    const int32_t lo = x - 64;
+    const int32_t wi = lo >> 5;
+    const uint32_t sh = (uint32_t)lo & 31;
+    const uint32_t w0 = arr[wi], w1 = arr[wi + 1], w2 = arr[wi + 2];
     return ((uint64_t)__funnelshift_r(w1, w2, sh) << 32) | __funnelshift_r(w0, w1, sh);
 }
+__device__ __forceinline__ bool cell6(const uint32_t* arr, int32_t k) { return (arr[k >> 5] >> (k & 31)) & 1; }
 
 // Per-thread K3 accumulators of one block (sums wrap mod 2^64).
 struct K3Acc {
@@ -492,16 +626,19 @@ struct K3Acc {
             mi = il;
         }
     }
+    __device__ __forceinline__ void add(uint32_t p, uint32_t il) {
+        sp += p;
+        spi += (uint64_t)p * il;
+        observe(p, il);
+    }
 };
 
-// Candidates z < ZBS (p <= 3 + 2(ZBS-1) = 257) are scanned bit-sliced, 32
-// evens per lane (gb_bitslice.cuh); the few evens left ("deep") continue
-// per even from window ZBS/64.
-constexpr uint32_t ZBS = 128;
-
-static_assert(E < (1u << 24), "deep queue entries pack il in 24 bits");
-constexpr int NPL = BS_SCAN128_PLANES;   // z planes
-constexpr uint32_t QCAP = 256;           // per-warp deep-even queue
+// Candidates p <= 257 are scanned bit-sliced (gb_bitslice.cuh bs6_scan_r*),
+// 32 class-r evens per lane; the few evens left ("deep") continue per even
+// over 64-wide windows of g = p div 6.
+constexpr uint32_t PBS = 257;
+constexpr int NPL = BS6_PLANES;          // z planes
+constexpr uint32_t QCAP = 512;           // per-warp deep-even queue (classes 2, 4 run ~2x the mean deep rate)
 
 // Straggler entry for an even with no candidate inside the in-tile halo.
 __device__ __forceinline__ void push_straggler(const VerifyArgs& A, const SegJob& J, uint32_t s, uint32_t iseg,
@@ -512,54 +649,91 @@ __device__ __forceinline__ void push_straggler(const VerifyArgs& A, const SegJob
     const uint32_t flags = ((uint64_t)JH <= jmax ? F_NEED_P1 : F_P1_FAIL) | extra_flags;
     const unsigned idx = atomicAdd(A.list_count, 1u);
     if (idx < A.list_cap) A.list[idx] = StragEntry{s, iseg, (uint32_t)JH, flags};
+    GB_STAT(4, 1);
 }
 
-// Deep even of a fast block: windows k = ZBS/64 .. NWIN-1 (one exit).
+// Per-class constants of a block: class ci holds the evens il = ci + 3t;
+// their n = r (mod 6), and candidate g reads cell t + G - g.
+struct Class6 {
+    uint32_t r, G;
+};
+__device__ __forceinline__ Class6 class6(const SegJob& J, uint32_t ci) {
+    return Class6{(uint32_t)((J.a + 2 * ci) % 6), (J.delta + 2 * ci) / 6};
+}
+// the three classes of a block, looked up without local memory
+struct Classes6 {
+    uint32_t r0, r1, r2, G0, G1, G2;
+    __device__ __forceinline__ explicit Classes6(const SegJob& J) {
+        const uint32_t a6 = (uint32_t)(J.a % 6);
+        r0 = a6;
+        r1 = (a6 + 2) % 6;
+        r2 = (a6 + 4) % 6;
+        G0 = J.delta / 6;
+        G1 = (J.delta + 2) / 6;
+        G2 = (J.delta + 4) / 6;
+    }
+    __device__ __forceinline__ Class6 operator[](uint32_t ci) const {
+        return Class6{ci == 0 ? r0 : ci == 1 ? r1 : r2, ci == 0 ? G0 : ci == 1 ? G1 : G2};
+    }
+};
+
+// Window j (g in [64j, 64j + 64)) of a class-r even t: smallest p with a hit
+// under the masks (0 = none).  r = 2: A, p = 6g + 1; r = 4: B, p = 6g - 1;
+// r = 0: A with p = 6g + 5 and B with p = 6g + 1.  lim1 / lim5 narrow the
+// masks (generic path).  The first read is selected, not branched, so a warp
+// whose entries mix classes does not walk every class's path.
+__device__ __forceinline__ uint32_t window_hit6(const uint32_t* tile, const uint64_t* masks6, uint32_t r, uint32_t G,
+                                               uint32_t t, uint32_t j, uint64_t lim1, uint64_t lim5m, uint64_t lim5p) {
+    const int32_t x = (int32_t)(t + G) - 64 * (int32_t)j + 1;
+    const uint32_t cls = r == 2 ? 0u : r == 4 ? 1u : 2u; // masks6 row: 6g+1, 6g-1, 6g+5
+    const uint64_t lim = r == 2 ? lim1 : r == 4 ? lim5m : lim5p;
+    const int32_t off = r == 2 ? 1 : r == 4 ? -1 : 5;
+    const uint64_t m = window6(r == 4 ? arr_b(tile) : arr_a(tile), x) & masks6[cls * NWIN6 + j] & lim;
+    uint32_t p = m ? (uint32_t)(6 * (int32_t)(64 * j + __clzll(m)) + off) : 0xFFFFFFFFu;
+    if (r == 0) {
+        const uint64_t mb = window6(arr_b(tile), x) & masks6[j] & lim1;
+        if (mb) p = min(p, 6 * (64 * j + __clzll(mb)) + 1);
+    }
+    return p == 0xFFFFFFFFu ? 0 : p;
+}
+
+// Deep even of a fast block in place (queue overflow): windows j0 .. NWIN6-1.
 template <bool PMIN>
-__device__ __forceinline__ void deep_even(const uint32_t* tile, const uint64_t* pmr, uint32_t il, uint32_t i0,
-                                          uint32_t s, const SegJob& J, const VerifyArgs& A, uint32_t jlim_small,
-                                          K3Acc& acc) {
-    const uint32_t x0 = (uint32_t)JH + il + 1;
-    uint32_t k = ZBS / 64;
-    uint64_t m = 0;
-#pragma unroll 1
-    for (; k < (uint32_t)NWIN; ++k) {
-        m = window_bits_hi(tile, x0 - 64 * k) & pmr[k];
-        if (m) break;
-    }
-    const uint32_t p = m ? 3 + 2 * (64 * k + __clzll(m)) : 0;
-    if (p) {
-        acc.sp += p;
-        acc.spi += (uint64_t)p * il;
-        acc.observe(p, il);
-    } else {
-        push_straggler(A, J, s, i0 + il, jlim_small, 0);
-    }
+__device__ __forceinline__ void deep_even6(const uint32_t* tile, const uint64_t* masks6, uint32_t t, const Class6 C,
+                                           uint32_t ci, uint32_t i0, uint32_t s, const SegJob& J,
+                                           const VerifyArgs& A, uint32_t jlim_small, K3Acc& acc) {
+    GB_STAT(1, 1);
+    uint32_t p = 0;
+    for (uint32_t j = 0; j < (uint32_t)NWIN6 && !p; ++j) p = window_hit6(tile, masks6, C.r, C.G, t, j, ~0ull, ~0ull, ~0ull);
+    const uint32_t il = ci + 3 * t;
+    if (p) acc.add(p, il);
+    else push_straggler(A, J, s, i0 + il, jlim_small, 0);
     if constexpr (PMIN) A.pmin_out[i0 + il] = p;
 }
 
-// One round over the warp's deep-even queue: the top n entries (il | k << 24)
-// each test ONE window k; misses are pushed back with k + 1, so no lane idles
-// while another walks many windows.  Returns the new queue length.
+// One round over the warp's deep-even queue: the top n entries
+// (t | ci << 18 | j << 20) each test ONE window j; misses are pushed back
+// with j + 1, so no lane idles while another walks many windows.
 template <bool PMIN>
-__device__ __forceinline__ uint32_t deep_round(const uint32_t* tile, const uint64_t* pmr, uint32_t* q, uint32_t qn,
-                                               uint32_t n, uint32_t lane, uint32_t i0, uint32_t s, const SegJob& J,
-                                               const VerifyArgs& A, uint32_t jlim_small, K3Acc& acc) {
+__device__ __forceinline__ uint32_t deep_round6(const uint32_t* tile, const uint64_t* masks6, uint32_t* q, uint32_t qn,
+                                                uint32_t n, uint32_t lane, uint32_t i0, uint32_t s, const SegJob& J,
+                                                const Classes6& CL, const VerifyArgs& A, uint32_t jlim_small,
+                                                K3Acc& acc) {
     qn -= n;
     const bool act = lane < n;
     const uint32_t e = act ? q[qn + lane] : 0u;
     __syncwarp();
+    if (lane == 0) GB_STAT(3, 1);
     bool again = false;
     if (act) {
-        const uint32_t il = e & 0xFFFFFFu, k = e >> 24;
-        const uint64_t m = window_bits_hi(tile, (uint32_t)JH + il + 1 - 64 * k) & pmr[k];
-        if (m) {
-            const uint32_t p = 3 + 2 * (64 * k + __clzll(m));
-            acc.sp += p;
-            acc.spi += (uint64_t)p * il;
-            acc.observe(p, il);
+        const uint32_t t = e & 0x3FFFFu, ci = (e >> 18) & 3u, j = e >> 20;
+        const Class6 C = CL[ci];
+        const uint32_t p = window_hit6(tile, masks6, C.r, C.G, t, j, ~0ull, ~0ull, ~0ull);
+        const uint32_t il = ci + 3 * t;
+        if (p) {
+            acc.add(p, il);
             if constexpr (PMIN) A.pmin_out[i0 + il] = p;
-        } else if (k + 1 < (uint32_t)NWIN) {
+        } else if (j + 1 < (uint32_t)NWIN6) {
             again = true;
         } else {
             push_straggler(A, J, s, i0 + il, jlim_small, 0);
@@ -567,43 +741,54 @@ __device__ __forceinline__ uint32_t deep_round(const uint32_t* tile, const uint6
         }
     }
     const uint32_t bal = __ballot_sync(0xffffffffu, again);
-    if (again) q[qn + __popc(bal & ((1u << lane) - 1))] = e + (1u << 24);
+    if (again) q[qn + __popc(bal & ((1u << lane) - 1))] = e + (1u << 20);
     __syncwarp();
     return qn + __popc(bal);
 }
 
-// Generic per-even check (low window, n = 4, q >= 3 limits, small p_small,
-// injected even, block tails): exact windows k < kmax.
+// bits m of window j with g = 64j + m <= gl (bit 63 - m)
+__device__ __forceinline__ uint64_t glim_mask(int64_t gl, uint32_t j) {
+    const int64_t mm = gl - 64 * (int64_t)j;
+    if (mm < 0) return 0;
+    if (mm >= 63) return ~0ull;
+    return ~0ull << (63 - mm);
+}
+
+// Generic per-even check (windows near the start of the number line, small
+// p_small, injected even): candidates p <= min(p_small, n - 3, PH6) in
+// ascending order, then the straggler list.
 template <bool PMIN>
-__device__ __forceinline__ void generic_even(const uint32_t* tile, const uint64_t* pmr, uint32_t il, uint32_t t0,
-                                             uint32_t i0, uint32_t s, const SegJob& J, const VerifyArgs& A,
-                                             uint32_t jlim_small, K3Acc& acc) {
+__device__ __forceinline__ void generic_even6(const uint32_t* tile, const uint64_t* masks6, uint32_t il,
+                                              uint32_t i0, uint32_t s, const SegJob& J, const VerifyArgs& A,
+                                              uint32_t jlim_small, K3Acc& acc) {
     const uint32_t iseg = i0 + il;
     const uint64_t n = J.a + 2ull * iseg;
     uint32_t p = 0;
     if (n == 4) {
         p = 2;
     } else {
-        const int64_t t = (int64_t)t0 + il;
-        const uint64_t jq = (n - 6) >> 1;
-        uint32_t jmax = jlim_small;
-        if (jq < jmax) jmax = (uint32_t)jq;
-        const uint32_t kmax = min((uint32_t)NWIN, jmax / 64 + 1);
-        for (uint32_t k = 0; k < kmax; ++k) {
-            const uint64_t m = window_bits(tile, t + 1 - 64 * (int64_t)k) & pmr[k];
-            if (m) {
-                p = 3 + 2 * (64 * k + __clzll(m));
-                break;
+        const uint32_t ci = il % 3, t = il / 3;
+        const Class6 C = class6(J, ci);
+        uint64_t pmax = n - 3;
+        if (pmax > A.p_small) pmax = A.p_small;
+        if (pmax > PH6) pmax = PH6;
+        if (pmax >= 3) {
+            if (n == 6) p = 3; // q = 3 has no cell
+            else if (C.r == 2 && cell6(arr_b(tile), (int32_t)(t + C.G) - 1)) p = 3;
+            else if (C.r == 4 && cell6(arr_a(tile), (int32_t)(t + C.G))) p = 3;
+        }
+        if (!p && pmax >= 5) {
+            const int64_t g1 = ((int64_t)pmax - 1) / 6, g5m = ((int64_t)pmax + 1) / 6, g5p = ((int64_t)pmax - 5) / 6;
+            for (uint32_t j = 0; j < (uint32_t)NWIN6 && !p; ++j) {
+                if (64 * (int64_t)j > g5m) break;
+                p = window_hit6(tile, masks6, C.r, C.G, t, j, glim_mask(g1, j), glim_mask(g5m, j),
+                                pmax >= 5 ? glim_mask(g5p, j) : 0);
             }
         }
-        // a hit beyond jmax cannot occur: pmr caps p_small and cells below
-        // q = 3 are zero (low window) or absent
         if (!p) push_straggler(A, J, s, iseg, jlim_small, n == A.inject ? F_INJECT : 0u);
     }
     if (p) {
-        acc.sp += p;
-        acc.spi += (uint64_t)p * il;
-        acc.observe(p, il);
+        acc.add(p, il);
         if (n == A.inject) {
             const unsigned idx = atomicAdd(A.list_count, 1u);
             if (idx < A.list_cap) A.list[idx] = StragEntry{s, iseg, 0u, F_INJECT | F_OBSERVED};
@@ -622,7 +807,8 @@ __device__ __forceinline__ uint32_t idx_sum(uint32_t x) {
 // sums of z (VPL planes), FC = per-position found counts (FPL planes);
 // p = 3 + 2z, so the sum is 2 sum_b 2^b idx(V_b) + 3 sum_k 2^k idx(FC_k).
 // Resets V and FC.
-constexpr uint32_t VACC = 4;
+constexpr uint32_t VACC = 4;  // words per compaction batch
+constexpr uint32_t VFLUSH = 4; // words per vertical-counter reduction
 constexpr int VPL = NPL + 2;   // 4 * 127 < 2^9
 constexpr int FPL = 3;         // 4 < 2^3
 __device__ __forceinline__ uint32_t vsum_by_index(uint32_t (&V)[VPL], uint32_t (&FC)[FPL]) {
@@ -640,16 +826,28 @@ __device__ __forceinline__ uint32_t vsum_by_index(uint32_t (&V)[VPL], uint32_t (
     return q;
 }
 
-// Bit-sliced scan of word w of a fast block: U = evens (bits) with no
-// candidate z < ZBS, F = ~U found, Z = planes of their z.
-__device__ __forceinline__ uint32_t scan_word(const uint32_t* tile, uint32_t w, uint32_t (&Z)[NPL]) {
-    const uint32_t* tp = tile + JH / 32 + w; // word B of the lane's top cells
-    uint32_t U = ~0u;
-    bs_scan128(tp[-4], tp[-3], tp[-2], tp[-1], tp[0], U, Z);
-    return U;
+// Bit-sliced scan of word w of class r: U in = valid evens of the word,
+// U out = those with no candidate p <= PBS; Z = planes of the found z.
+__device__ __forceinline__ void scan_word6(const uint32_t* tile, uint32_t r, uint32_t WB, uint32_t& U,
+                                           uint32_t (&Z)[NPL]) {
+    const uint32_t* a = arr_a(tile) + WB;
+    const uint32_t* b = arr_b(tile) + WB;
+    const uint32_t a0 = a[-2], a1 = a[-1], a2 = a[0], b0 = b[-2], b1 = b[-1], b2 = b[0];
+    if (r == 0) bs6_scan_r0(a0, a1, a2, b0, b1, b2, U, Z);
+    else if (r == 2) bs6_scan_r2(a0, a1, a2, b0, b1, b2, U, Z);
+    else bs6_scan_r4(a0, a1, a2, b0, b1, b2, U, Z);
 }
 
-// Barrier of one group of GT threads (id 0 with GT = the CTA size: __syncthreads).
+// Valid bits of word w of a class with T evens and alignment delta.
+__device__ __forceinline__ uint32_t word_mask6(uint32_t w, uint32_t T, uint32_t delta) {
+    uint32_t m = ~0u;
+    if (w == 0) m <<= delta;
+    const int64_t hi = (int64_t)T + delta - 32 * (int64_t)w; // bits < hi valid
+    if (hi < 32) m &= hi <= 0 ? 0u : (1u << hi) - 1;
+    return m;
+}
+
+// Barrier of one group of GT threads.
 template <int GT>
 __device__ __forceinline__ void gbar(int id) { asm volatile("bar.sync %0, %1;" ::"r"(id), "n"(GT) : "memory"); }
 __device__ __forceinline__ void nb_sync(int id, int n) { asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory"); }
@@ -658,10 +856,10 @@ __device__ __forceinline__ void nb_arrive(int id, int n) { asm volatile("bar.arr
 // Where flat block fb of a batch lies: slot, block of the slot, window.
 struct BlockInfo {
     SegJob J;
-    uint64_t q_w;   // q of the window's cell 0
     uint32_t s, b;  // slot, block index within the slot
-    uint32_t B;     // window start cell relative to the slot's qbase
-    bool low;       // window at q = 1
+    uint32_t KB;    // window start cell relative to the slot's origin (b K6)
+    bool low;       // window origin <= sbound: fix-up needed
+    int64_t Qs;     // window origin (valid when low)
 };
 
 __device__ __forceinline__ BlockInfo block_info(const VerifyArgs& A, uint32_t fb) {
@@ -671,164 +869,210 @@ __device__ __forceinline__ BlockInfo block_info(const VerifyArgs& A, uint32_t fb
     I.s = s;
     I.J = A.jobs[s];
     I.b = fb - I.J.block_prefix;
-    I.low = I.b < I.J.b1;
-    I.q_w = I.low ? 1ull : I.J.qbase + 2ull * (uint64_t)(I.b - I.J.b1) * E;
-    I.B = I.low ? 0u : (I.b - I.J.b1) * E;
+    I.KB = I.b * K6;
+    const uint64_t off = 6ull * I.KB;
+    if (I.J.qneg) {
+        I.Qs = (int64_t)off - (int64_t)I.J.qbase;
+        I.low = I.Qs <= (int64_t)A.sbound;
+    } else {
+        I.low = I.J.qbase <= A.sbound && off <= A.sbound - I.J.qbase;
+        I.Qs = I.low ? (int64_t)(I.J.qbase + off) : 0;
+    }
     return I;
 }
 
 // K2: sieve block I into tile by one group (tid = index in the group).  On
-// return this thread's strikes are issued; the caller's barrier publishes.
+// return this thread's strikes and fix-ups are issued; the caller's barrier
+// publishes them.
 template <int GT>
-__device__ __forceinline__ void sieve_block(const VerifyArgs& A, uint32_t* tile, const uint32_t* pat,
+__device__ __forceinline__ void sieve_block(const VerifyArgs& A, uint32_t* tile, const uint32_t* pat6,
                                             const BlockInfo& I, uint32_t tid, int bar) {
-    presieve_window(tile, pat, I.q_w, tid, GT);
+    uint32_t pha[4], phb[4];
+#pragma unroll
+    for (int g = 0; g < 4; ++g) {
+        const uint32_t P = pg6_p(g), iv = inv6_mod(P);
+        const uint32_t qm = (uint32_t)((I.J.qmod[g] + 6ull * (I.KB % P)) % P); // Q_b mod P
+        pha[g] = (uint32_t)((uint64_t)((qm + P - 1) % P) * iv % P);            // (Q_b - 1)/6
+        phb[g] = (uint32_t)((uint64_t)((qm + 3) % P) * iv % P);                // (Q_b + 3)/6
+    }
+    presieve6(arr_a(tile), pat6, pha, tid, GT);
+    presieve6(arr_b(tile), pat6, phb, tid, GT);
     gbar<GT>(bar);
-    presieve_fixup(tile, I.q_w, tid);
-    strike_verify<GT>(tile, A.pmc + (size_t)I.s * A.np, A.iA1 - A.iA0, A.iW1 - A.iA0, A.iB1 - A.iA0, I.B, I.low,
-                  tid, A.wsplit);
-    if (A.qg != nullptr && !I.low && I.J.qg_words) {
+    strike_verify6<GT>(tile, A.pmc + (size_t)I.s * A.np, A.iA1 - A.iA0, A.iW1 - A.iA0, A.iB1 - A.iA0, I.KB, tid,
+                       A.wsplit);
+    if (A.qg != nullptr && I.J.qg_words) {
         gbar<GT>(bar);
-        const uint32_t* g = A.qg + I.s * A.qg_stride_words + I.B / 32;
-        const uint32_t lim = min((uint32_t)TILE_WORDS, I.J.qg_words - I.B / 32);
-        for (uint32_t wd = tid; wd < lim; wd += GT) tile[wd] &= __ldg(g + wd);
+        const uint32_t* ga = A.qg + I.s * A.qg_stride_words + I.KB / 32;
+        const uint32_t* gb = ga + I.J.qg_words;
+        const uint32_t lim = min(M6W, I.J.qg_words - I.KB / 32);
+        uint32_t* ta = arr_a(tile);
+        uint32_t* tb = arr_b(tile);
+        for (uint32_t wd = tid; wd < lim; wd += GT) {
+            ta[wd] &= __ldg(ga + wd);
+            tb[wd] &= __ldg(gb + wd);
+        }
+    }
+    if (I.low) {
+        gbar<GT>(bar);
+        fixup_low6(tile, I.Qs, A.primes, A.n_primes, A.sbound, tid, GT);
     }
 }
 
 // K3: minimal p of every even of block I over the sieved tile, by one group;
 // the block's sums / max key go to the slot accumulators.
 template <bool PMIN, int GT>
-__device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t* tile, const uint64_t* pmr,
+__device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t* tile, const uint64_t* masks6,
                                             const BlockInfo& I, uint32_t tid, int bar,
                                             unsigned long long (*s_red)[3], unsigned long long* s_key_p,
                                             uint32_t (*s_q)[QCAP]) {
     const uint32_t lane = tid & 31, warp = tid >> 5;
     const uint32_t jlim_small = A.p_small >= 3 ? (uint32_t)min((A.p_small - 3) / 2, (uint64_t)0xFFFFFFFFu) : 0;
-    const uint32_t s = I.s, b = I.b;
+    const uint32_t s = I.s;
     const SegJob& J = I.J;
-    const bool low = I.low;
     unsigned long long& s_key = *s_key_p;
-    // ---- K3: minimal p per even, while the tile is in shared memory
-    const uint32_t i0 = b * E;
-    const uint32_t ne = min(E, J.evens - i0);
+    const uint32_t i0 = I.b * E6;
+    const uint32_t ne = min(E6, J.evens - i0);
     const uint64_t n_first = J.a + 2ull * i0, n_last = n_first + 2ull * (ne - 1);
     const bool inject_here = (A.inject & 1) == 0 && A.inject >= n_first && A.inject <= n_last;
-    // fast blocks: every even has all NWIN windows valid (n >= 8196,
-    // p_small >= 8193), no n = 4, no injected even
-    const bool fast = !low && jlim_small >= (uint32_t)JH - 1 && !inject_here;
+    // fast blocks: every even has all candidates p <= PH6 valid (n >= PH6 + 3,
+    // p_small >= PH6), no n = 4, no injected even
+    const bool fast = n_first >= PH6 + 3 && jlim_small >= (uint32_t)JH - 1 && !inject_here;
     K3Acc acc;
-    const uint32_t nw = fast ? ne >> 5 : 0; // full words of the fast path
+    if (fast && tid == 0) GB_STAT(5, 1);
     if (fast) {
         uint32_t* q = s_q[warp];
-        uint32_t qn = 0;  // warp-uniform queue length (< 32 between words)
+        uint32_t qn = 0;   // warp-uniform queue length (< 32 between batches)
         uint32_t sp32 = 0; // sum p of the bit-sliced evens (< 2^32 per lane)
-        // sum p * (bit index) is deferred: z planes and found bits of up
-        // to VACC words are summed per bit position as bit-sliced
-        // counters V (z) and FC (found), then reduced by bit index once
+        // sum p * (bit index) is deferred: z planes and found bits of VACC
+        // words are summed per bit position as bit-sliced counters V (z) and
+        // FC (found), then reduced by bit index once
         uint32_t V[VPL], FC[FPL];
 #pragma unroll
         for (int k = 0; k < VPL; ++k) V[k] = 0;
 #pragma unroll
         for (int k = 0; k < FPL; ++k) FC[k] = 0;
-        // VACC words per lane per step (w = wb + k GT + lane): their
-        // vertical counters are reduced and their deep evens compacted once
-        for (uint32_t wb = warp * 32; wb < nw; wb += VACC * GT) {
-            uint32_t U[VACC];
+        const Classes6 CL(J);
+        uint32_t nbatch = 0; // batches in the vertical counters
+        for (uint32_t ci = 0; ci < 3; ++ci) {
+            const Class6 C = CL[ci];
+            const uint32_t T = ne > ci ? (ne - ci + 2) / 3 : 0;
+            const uint32_t delta = C.G & 31;
+            const uint32_t nw = (T + delta + 31) >> 5;
+            for (uint32_t wb = warp * 32; wb < nw; wb += VACC * GT) {
+                // the scan is not unrolled over the VACC words (code size:
+                // the three class scans must stay in the instruction cache);
+                // the words' leftovers go to named registers by select
+                uint32_t U[VACC];
 #pragma unroll
-            for (uint32_t k = 0; k < VACC; ++k) {
-                const uint32_t w = wb + k * GT + lane;
-                U[k] = 0;
-                if (w < nw) {
-                    uint32_t Z[NPL];
-                    U[k] = scan_word(tile, w, Z);
-                    const uint32_t F = ~U[k];
-                    // p = 3 + 2z: sum p of the word (weight 32w below)
-                    uint32_t P = 3 * __popc(F);
-#pragma unroll
-                    for (int bp = 0; bp < NPL; ++bp) P += (2u << bp) * __popc(Z[bp]);
-                    sp32 += P;
-                    acc.spi += (uint64_t)(32 * w) * P;
-                    // V += Z, FC += F (ripple-carry, bit-sliced)
-                    uint32_t cy = V[0] & Z[0];
-                    V[0] ^= Z[0];
-#pragma unroll
-                    for (int bp = 1; bp < NPL; ++bp) {
-                        const uint32_t v = V[bp], z = Z[bp];
-                        V[bp] = v ^ z ^ cy;
-                        cy = (v & z) | (cy & (v ^ z));
-                    }
-#pragma unroll
-                    for (int bp = NPL; bp < VPL; ++bp) {
-                        const uint32_t v = V[bp];
-                        V[bp] = v ^ cy;
-                        cy = v & cy;
-                    }
-                    cy = F;
-#pragma unroll
-                    for (int kk = 0; kk < FPL; ++kk) {
-                        const uint32_t f = FC[kk];
-                        FC[kk] = f ^ cy;
-                        cy = f & cy;
-                    }
-                    if constexpr (PMIN) {
-                        for (uint32_t i = 0; i < 32; ++i) {
-                            if (!((F >> i) & 1)) continue;
-                            uint32_t z = 0;
-#pragma unroll
-                            for (int bp = 0; bp < NPL; ++bp) z |= ((Z[bp] >> i) & 1) << bp;
-                            A.pmin_out[i0 + 32 * w + i] = 3 + 2 * z;
-                        }
-                    }
-                }
-            }
-            acc.spi += vsum_by_index(V, FC);
-            // deep evens of the VACC words: compact into the warp queue with
-            // one warp prefix sum, drain 32 at a time
-            uint32_t cnt = 0;
-#pragma unroll
-            for (uint32_t k = 0; k < VACC; ++k) cnt += __popc(U[k]);
-            uint32_t incl = cnt;
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                if (lane >= (uint32_t)o) incl += y;
-            }
-            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-            if (qn + total <= QCAP) {
-                uint32_t pos = qn + incl - cnt;
-#pragma unroll
+                for (uint32_t k = 0; k < VACC; ++k) U[k] = 0;
+#pragma unroll 1
                 for (uint32_t k = 0; k < VACC; ++k) {
                     const uint32_t w = wb + k * GT + lane;
-                    while (U[k]) {
-                        const uint32_t bit = __ffs(U[k]) - 1;
-                        U[k] &= U[k] - 1;
-                        q[pos++] = (32 * w + bit) | ((ZBS / 64) << 24);
-                    }
-                }
-                qn += total;
-                __syncwarp();
-                while (qn >= 32) qn = deep_round<PMIN>(tile, pmr, q, qn, 32, lane, i0, s, J, A, jlim_small, acc);
-            } else {
+                    uint32_t Uk = 0;
+                    if (w < nw) {
+                        const uint32_t valid = (w == 0 || w + 1 == nw) ? word_mask6(w, T, delta) : ~0u;
+                        uint32_t Z[NPL];
+                        Uk = valid;
+                        scan_word6(tile, C.r, w + (C.G >> 5), Uk, Z);
+                        const uint32_t F = valid & ~Uk;
+                        // p = 3 + 2z: sum p of the word; il = ci + 3 (32w - delta + i)
+                        uint32_t P = 3 * __popc(F);
 #pragma unroll
-                for (uint32_t k = 0; k < VACC; ++k) { // queue full: this lane's deep evens in place
-                    const uint32_t w = wb + k * GT + lane;
-                    while (U[k]) {
-                        const uint32_t bit = __ffs(U[k]) - 1;
-                        U[k] &= U[k] - 1;
-                        deep_even<PMIN>(tile, pmr, 32 * w + bit, i0, s, J, A, jlim_small, acc);
+                        for (int bp = 0; bp < NPL; ++bp) P += (2u << bp) * __popc(Z[bp]);
+                        sp32 += P;
+                        acc.spi += (uint64_t)P * (uint64_t)((int64_t)ci + 96 * (int64_t)w - 3 * (int64_t)delta);
+                        // V += Z, FC += F (ripple-carry, bit-sliced)
+                        uint32_t cy = V[0] & Z[0];
+                        V[0] ^= Z[0];
+#pragma unroll
+                        for (int bp = 1; bp < NPL; ++bp) {
+                            const uint32_t v = V[bp], z = Z[bp];
+                            V[bp] = v ^ z ^ cy;
+                            cy = (v & z) | (cy & (v ^ z));
+                        }
+#pragma unroll
+                        for (int bp = NPL; bp < VPL; ++bp) {
+                            const uint32_t v = V[bp];
+                            V[bp] = v ^ cy;
+                            cy = v & cy;
+                        }
+                        cy = F;
+#pragma unroll
+                        for (int kk = 0; kk < FPL; ++kk) {
+                            const uint32_t f = FC[kk];
+                            FC[kk] = f ^ cy;
+                            cy = f & cy;
+                        }
+                        if constexpr (PMIN) {
+                            for (uint32_t i = 0; i < 32; ++i) {
+                                if (!((F >> i) & 1)) continue;
+                                uint32_t z = 0;
+#pragma unroll
+                                for (int bp = 0; bp < NPL; ++bp) z |= ((Z[bp] >> i) & 1) << bp;
+                                A.pmin_out[i0 + ci + 3 * (32 * w - delta + i)] = 3 + 2 * z;
+                            }
+                        }
                     }
+#pragma unroll
+                    for (uint32_t kk = 0; kk < VACC; ++kk)
+                        if (kk == k) U[kk] = Uk;
                 }
-                __syncwarp();
+                if (++nbatch == VFLUSH / VACC) { // counters hold VFLUSH words
+                    acc.spi += 3ull * vsum_by_index(V, FC);
+                    nbatch = 0;
+                }
+                // deep evens of the VACC words: compact into the warp queue with
+                // one warp prefix sum, drain 32 at a time
+                uint32_t cnt = 0;
+#pragma unroll
+                for (uint32_t k = 0; k < VACC; ++k) cnt += __popc(U[k]);
+                uint32_t incl = cnt;
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+                    if (lane >= (uint32_t)o) incl += y;
+                }
+                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                if (lane == 0) GB_STAT(2, total);
+                if (qn + total <= QCAP) {
+                    uint32_t pos = qn + incl - cnt;
+#pragma unroll
+                    for (uint32_t k = 0; k < VACC; ++k) {
+                        const uint32_t w = wb + k * GT + lane;
+                        while (U[k]) {
+                            const uint32_t bit = __ffs(U[k]) - 1;
+                            U[k] &= U[k] - 1;
+                            q[pos++] = (32 * w - delta + bit) | (ci << 18);
+                        }
+                    }
+                    qn += total;
+                    __syncwarp();
+                    while (qn >= 32)
+                        qn = deep_round6<PMIN>(tile, masks6, q, qn, 32, lane, i0, s, J, CL, A, jlim_small, acc);
+                } else {
+#pragma unroll
+                    for (uint32_t k = 0; k < VACC; ++k) { // queue full: this lane's deep evens in place
+                        const uint32_t w = wb + k * GT + lane;
+                        while (U[k]) {
+                            const uint32_t bit = __ffs(U[k]) - 1;
+                            U[k] &= U[k] - 1;
+                            deep_even6<PMIN>(tile, masks6, 32 * w - delta + bit, CL[ci], ci, i0, s, J, A, jlim_small,
+                                             acc);
+                        }
+                    }
+                    __syncwarp();
+                }
             }
         }
-        while (qn) qn = deep_round<PMIN>(tile, pmr, q, qn, min(qn, 32u), lane, i0, s, J, A, jlim_small, acc);
+        while (qn) qn = deep_round6<PMIN>(tile, masks6, q, qn, min(qn, 32u), lane, i0, s, J, CL, A, jlim_small, acc);
+        if (nbatch) acc.spi += 3ull * vsum_by_index(V, FC);
         acc.sp += sp32;
-    }
-    {
-        // generic path (whole block, or the tail of a fast block)
-        const uint32_t t0 = low ? (uint32_t)((J.a - 4) >> 1) : (uint32_t)JH;
-        for (uint32_t il = 32 * nw + tid; il < ne; il += GT)
-            generic_even<PMIN>(tile, pmr, il, t0, i0, s, J, A, jlim_small, acc);
+    } else {
+        if (tid == 0) GB_STAT(6, 1);
+        if (tid == 0) GB_STAT(0, ne);
+#ifndef GB_NO_GENERIC
+        for (uint32_t il = tid; il < ne; il += GT) generic_even6<PMIN>(tile, masks6, il, i0, s, J, A, jlim_small, acc);
+#endif
     }
     // ---- block reduction -> slot accumulators; key = p << 32 | ~iseg
     uint64_t key = acc.mp ? (((uint64_t)acc.mp << 32) | (0xFFFFFFFFu - (i0 + acc.mi))) : 0;
@@ -847,7 +1091,7 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
     gbar<GT>(bar);
     if (tid == 0) {
         uint64_t S = 0, SPI = 0, K = 0;
-        for (int w = 0; w < (GT / 32); ++w) {
+        for (int w = 0; w < GT / 32; ++w) {
             S += s_red[w][0];
             SPI += s_red[w][1];
             K = s_red[w][2] > K ? s_red[w][2] : K;
@@ -858,29 +1102,35 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
     }
     gbar<GT>(bar);
     uint64_t K = s_key;
-    if (nw && K < ((uint64_t)(3 + 2 * ZBS) << 32)) {
+    if (fast && K < ((uint64_t)(PBS + 2) << 32)) {
         // no deep even beat the bit-sliced range: the block max may be a
         // bit-sliced even -- rescan for max z (smallest il on ties)
         uint32_t bz = 0, bi = 0xFFFFFFFFu;
-        for (uint32_t wb = warp * 32; wb < nw; wb += GT) {
-            const uint32_t w = wb + lane;
-            if (w >= nw) continue;
-            uint32_t Z[NPL];
-            uint32_t cand = ~scan_word(tile, w, Z);
-            if (!cand) continue;
-            uint32_t mz = 0;
+        for (uint32_t ci = 0; ci < 3; ++ci) {
+            const Class6 C = class6(J, ci);
+            const uint32_t T = ne > ci ? (ne - ci + 2) / 3 : 0;
+            const uint32_t delta = C.G & 31;
+            const uint32_t nw = (T + delta + 31) >> 5;
+            for (uint32_t w = tid; w < nw; w += GT) {
+                const uint32_t valid = word_mask6(w, T, delta);
+                uint32_t U = valid, Z[NPL];
+                scan_word6(tile, C.r, w + (C.G >> 5), U, Z);
+                uint32_t cand = valid & ~U;
+                if (!cand) continue;
+                uint32_t mz = 0;
 #pragma unroll
-            for (int bp = NPL - 1; bp >= 0; --bp) {
-                const uint32_t t = cand & Z[bp];
-                if (t) {
-                    cand = t;
-                    mz |= 1u << bp;
+                for (int bp = NPL - 1; bp >= 0; --bp) {
+                    const uint32_t tt = cand & Z[bp];
+                    if (tt) {
+                        cand = tt;
+                        mz |= 1u << bp;
+                    }
                 }
-            }
-            const uint32_t il = 32 * w + __ffs(cand) - 1;
-            if (bi == 0xFFFFFFFFu || mz > bz) { // words ascend per lane: ties keep the smaller il
-                bz = mz;
-                bi = il;
+                const uint32_t il = ci + 3 * (32 * w - delta + __ffs(cand) - 1);
+                if (bi == 0xFFFFFFFFu || mz > bz || (mz == bz && il < bi)) {
+                    bz = mz;
+                    bi = il;
+                }
             }
         }
         uint64_t kf = bi != 0xFFFFFFFFu ? (((uint64_t)(3 + 2 * bz) << 32) | (0xFFFFFFFFu - (i0 + bi))) : 0;
@@ -895,62 +1145,29 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
     if (tid == 0 && K) atomicMax(&A.acc[s].key, (unsigned long long)K);
 }
 
-// Fused sieve + check, one 512-thread CTA per block at a time (2 per SM).
-template <bool PMIN>
-__global__ void __launch_bounds__(THREADS, CTAS_PER_SM) k_verify_blocks(VerifyArgs A) {
-    extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t* tile = smem;                                  // TILE_WORDS + pad
-    uint32_t* pat = smem + VERIFY_PAT_OFF;                  // PAT_WORDS
-    uint64_t* pmr = (uint64_t*)(smem + VERIFY_PMR_OFF);     // NWIN
-    __shared__ uint32_t s_blk;
-    __shared__ unsigned long long s_red[NWARPS][3];
-    __shared__ unsigned long long s_key;
-    __shared__ uint32_t s_q[NWARPS][QCAP];       // deep-even queue (block even indices)
-
-    for (uint32_t i = threadIdx.x; i < PAT_WORDS; i += blockDim.x) pat[i] = A.gpat[i];
-    for (uint32_t i = threadIdx.x; i < (uint32_t)NWIN; i += blockDim.x) pmr[i] = A.pmr[i];
-    for (uint32_t i = threadIdx.x; i < 4; i += blockDim.x) tile[TILE_WORDS + i] = 0;
-    // block claims: thread 0 requests the next block as soon as the current
-    // one starts, so the global atomic's round trip overlaps the sieve
-    uint32_t fb_next = 0;
-    if (threadIdx.x == 0) fb_next = atomicAdd(A.block_counter, 1u);
-    for (;;) {
-        if (threadIdx.x == 0) s_blk = fb_next;
-        __syncthreads();
-        const uint32_t fb = s_blk;
-        if (fb >= A.total_blocks) break;
-        if (threadIdx.x == 0) fb_next = atomicAdd(A.block_counter, 1u);
-        const BlockInfo I = block_info(A, fb);
-        sieve_block<THREADS>(A, tile, pat, I, threadIdx.x, 0);
-        __syncthreads();
-        check_block<PMIN, THREADS>(A, tile, pmr, I, threadIdx.x, 0, s_red, &s_key, s_q);
-    }
-}
-
-// Warp-specialised fused kernel: one 1024-thread CTA per SM, two tile
-// buffers.  The first WS_ST threads (the sieve group) sieve block k into
-// buffer k & 1 while the other WS_CT threads (the check group) check block
-// k - 1 in the other buffer.  Named barriers hand buffers over: FULL[b]
-// (sieve arrives, check waits) and EMPTY[b] (check arrives, sieve waits), so
-// the atomic-heavy sieve and the ALU-heavy check overlap instead of
-// alternating at CTA barriers.  The split is tuned so neither group waits.
+// Warp-specialised fused kernel: one 1024-thread CTA per SM, two wheel-6
+// tile buffers.  The first WS_ST threads (the sieve group) sieve block k
+// into buffer k & 1 while the other WS_CT threads (the check group) check
+// block k - 1 in the other buffer.  Named barriers hand buffers over:
+// FULL[b] (sieve arrives, check waits) and EMPTY[b] (check arrives, sieve
+// waits), so the atomic-heavy sieve and the ALU-heavy check overlap instead
+// of alternating at CTA barriers.
 constexpr int BAR_S = 1, BAR_C = 2, BAR_FULL = 3, BAR_EMPTY = 5; // FULL/EMPTY + buffer
-constexpr uint32_t WS_TILE_STRIDE = TILE_WORDS + 4;
 
 template <bool PMIN>
 __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
     extern __shared__ __align__(16) uint32_t smem[];
-    uint32_t* tiles = smem;                                 // 2 x WS_TILE_STRIDE
-    uint32_t* pat = smem + WS_PAT_OFF;                      // PAT_WORDS
-    uint64_t* pmr = (uint64_t*)(smem + WS_PMR_OFF);         // NWIN
+    uint32_t* tiles = smem;                                 // 2 x TILE6_WORDS
+    uint32_t* pat6 = smem + WS_PAT_OFF;                     // PAT6_WORDS
+    uint64_t* masks6 = (uint64_t*)(smem + WS_MASK_OFF);     // 3 x NWIN6
     __shared__ uint32_t s_fb[2];
     __shared__ unsigned long long s_red[WS_CT / 32][3];
     __shared__ unsigned long long s_key;
     __shared__ uint32_t s_q[WS_CT / 32][QCAP];
 
-    for (uint32_t i = threadIdx.x; i < PAT_WORDS; i += blockDim.x) pat[i] = A.gpat[i];
-    for (uint32_t i = threadIdx.x; i < (uint32_t)NWIN; i += blockDim.x) pmr[i] = A.pmr[i];
-    for (uint32_t i = threadIdx.x; i < 8; i += blockDim.x) tiles[(i >> 2) * WS_TILE_STRIDE + TILE_WORDS + (i & 3)] = 0;
+    for (uint32_t i = threadIdx.x; i < PAT6_WORDS; i += blockDim.x) pat6[i] = A.gpat6[i];
+    for (uint32_t i = threadIdx.x; i < 3u * NWIN6; i += blockDim.x) masks6[i] = A.masks6[i];
+    for (uint32_t i = threadIdx.x; i < 2 * TILE6_WORDS; i += blockDim.x) tiles[i] = 0; // pads stay zero
     __syncthreads();
     const int NB = WS_THREADS; // participants of FULL / EMPTY
     if (threadIdx.x < WS_ST) {
@@ -960,7 +1177,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
         if (tid == 0) fb_next = atomicAdd(A.block_counter, 1u);
         for (uint32_t k = 0;; ++k) {
             const uint32_t bs = k & 1;
-            uint32_t* tile = tiles + bs * WS_TILE_STRIDE;
+            uint32_t* tile = tiles + bs * TILE6_WORDS;
             if (k >= 2) nb_sync(BAR_EMPTY + bs, NB); // check group done with block k - 2
             if (tid == 0) s_fb[bs] = fb_next;
             gbar<WS_ST>(BAR_S);
@@ -972,7 +1189,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
             }
             if (tid == 0) fb_next = atomicAdd(A.block_counter, 1u);
             const BlockInfo I = block_info(A, fb);
-            sieve_block<WS_ST>(A, tile, pat, I, tid, BAR_S);
+#ifndef GB_SKIP_SIEVE // timing probe: check group alone (on stale tiles)
+            sieve_block<WS_ST>(A, tile, pat6, I, tid, BAR_S);
+#endif
             nb_arrive(BAR_FULL + bs, NB);
         }
     } else {
@@ -984,7 +1203,9 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
             const uint32_t fb = s_fb[bs];
             if (fb >= A.total_blocks) return;
             const BlockInfo I = block_info(A, fb);
-            check_block<PMIN, WS_CT>(A, tiles + bs * WS_TILE_STRIDE, pmr, I, tid, BAR_C, s_red, &s_key, s_q);
+#ifndef GB_SKIP_CHECK // timing probe: sieve group alone
+            check_block<PMIN, WS_CT>(A, tiles + bs * TILE6_WORDS, masks6, I, tid, BAR_C, s_red, &s_key, s_q);
+#endif
             nb_arrive(BAR_EMPTY + bs, NB);
         }
     }
@@ -1163,6 +1384,21 @@ __global__ void __launch_bounds__(SMEM_PEAK_THREADS, 2) k_smem_peak(uint32_t ite
 }
 
 // ============================================================ launchers
+int debug_stats(unsigned long long* out, int reset) {
+#ifdef GB_STATS
+    if (cudaMemcpyFromSymbol(out, g_stats, sizeof(g_stats)) != cudaSuccess) return 1;
+    if (reset) {
+        unsigned long long z[8] = {0, 0, 0, 0, 0, 0, 0, 0};
+        cudaMemcpyToSymbol(g_stats, z, sizeof(z));
+    }
+    return 0;
+#else
+    for (int i = 0; i < 8; ++i) out[i] = 0;
+    (void)reset;
+    return 2;
+#endif
+}
+
 cudaError_t launch_smem_peak(uint32_t iters, uint32_t* sink, int grid, cudaStream_t st) {
     static bool attr = false;
     if (!attr) {
@@ -1172,8 +1408,9 @@ cudaError_t launch_smem_peak(uint32_t iters, uint32_t* sink, int grid, cudaStrea
     k_smem_peak<<<grid, SMEM_PEAK_THREADS, 65536, st>>>(iters, sink);
     return cudaGetLastError();
 }
-cudaError_t launch_init_tables(uint32_t* pat, uint64_t* pmr, uint64_t p_small, cudaStream_t st) {
-    k_init_tables<<<64, 256, 0, st>>>(pat, pmr, p_small);
+cudaError_t launch_init_tables(uint32_t* pat, uint64_t* pmr, uint32_t* pat6, uint64_t* masks6, uint64_t p_small,
+                               cudaStream_t st) {
+    k_init_tables<<<64, 256, 0, st>>>(pat, pmr, pat6, masks6, p_small);
     return cudaGetLastError();
 }
 cudaError_t launch_seed_primes(uint32_t lim, uint32_t* out, uint32_t* count, cudaStream_t st) {
@@ -1224,17 +1461,10 @@ cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint3
     return cudaGetLastError();
 }
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st) {
-#if GB_WS
     if (a.pmin_out)
         k_verify_ws<true><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
     else
         k_verify_ws<false><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
-#else
-    if (a.pmin_out)
-        k_verify_blocks<true><<<grid, THREADS, VERIFY_SMEM, st>>>(a);
-    else
-        k_verify_blocks<false><<<grid, THREADS, VERIFY_SMEM, st>>>(a);
-#endif
     return cudaGetLastError();
 }
 cudaError_t launch_stragglers(const SegJob* jobs, const StragEntry* list, const unsigned int* list_count,
@@ -1261,16 +1491,9 @@ cudaError_t launch_is_prime_batch(const uint64_t* v, uint8_t* out, uint64_t n, c
 }
 int verify_occupancy(int* blocks_per_sm) {
     // per-device function attributes: call after cudaSetDevice
-    if (cudaFuncSetAttribute(k_verify_blocks<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)VERIFY_SMEM) != cudaSuccess)
-        return 1;
-    if (cudaFuncSetAttribute(k_verify_blocks<true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                             (int)VERIFY_SMEM) != cudaSuccess)
-        return 1;
     if (cudaFuncSetAttribute(k_sieve_interval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SIEVE_SMEM) !=
         cudaSuccess)
         return 1;
-#if GB_WS
     if (cudaFuncSetAttribute(k_verify_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_SMEM) !=
         cudaSuccess)
         return 1;
@@ -1279,10 +1502,6 @@ int verify_occupancy(int* blocks_per_sm) {
         return 1;
     return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_verify_ws<false>, WS_THREADS,
                                                               WS_SMEM);
-#else
-    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_verify_blocks<false>, THREADS,
-                                                              VERIFY_SMEM);
-#endif
 }
 
 } // namespace gbk

@@ -25,16 +25,18 @@ struct VerifyArgs {
     const SegJob* jobs;
     uint32_t nslots;
     uint32_t total_blocks;
-    const uint32_t* primes;
+    const uint32_t* primes;       // all base primes (low-window fix-up)
+    uint64_t n_primes;
+    uint64_t sbound;              // max(sqrt bound, 47): windows starting at or below need the fix-up
     uint32_t iA0, iA1, iB1;       // tile prime index ranges
-    uint32_t iW1;                 // first tile prime >= W (strikes a block at most once)
+    uint32_t iW1;                 // first tile prime >= M6 (strikes an array at most once)
     uint32_t np;                  // pmc row length (iB1 - iA0)
-    const uint4* pmc;             // nslots * np {p, floor(2^32/p), p - 1 - c0, c0}
+    const uint4* pmc;             // nslots * np {p, floor(2^32/p), p - 1 - k0, 4 6^-1 mod p}
     const uint16_t* wsplit;       // [SPLIT_WARPS][32] warp-cooperative row indices (0xFFFF = none)
-    const uint32_t* qg;           // large-prime bitmask (nullptr = none)
+    const uint32_t* qg;           // large-prime wheel-6 bitmask (nullptr = none)
     uint64_t qg_stride_words;
-    const uint32_t* gpat;
-    const uint64_t* pmr;
+    const uint32_t* gpat6;        // wheel-6 presieve patterns
+    const uint64_t* masks6;       // 3 x NWIN6 deep-window prime masks
     uint64_t p_small;
     uint64_t inject;
     unsigned int* block_counter;
@@ -46,18 +48,15 @@ struct VerifyArgs {
 };
 
 // dynamic shared memory of the tile kernels
-// k_verify_blocks dynamic smem: [tile | 4 pad words][patterns][pmr (8-B aligned)]
-constexpr uint32_t VERIFY_PAT_OFF = TILE_WORDS + 4;
-constexpr uint32_t VERIFY_PMR_OFF = (VERIFY_PAT_OFF + PAT_WORDS + 3) & ~3u; // 16-B aligned, in words
-constexpr size_t VERIFY_SMEM = (size_t)VERIFY_PMR_OFF * 4 + NWIN * 8;
 constexpr size_t SIEVE_SMEM = (TILE_WORDS + 1 + PAT_WORDS) * 4;
-// k_verify_ws dynamic smem: [tile 0 | 4 pad][tile 1 | 4 pad][patterns][pmr]
-constexpr uint32_t WS_PAT_OFF = 2 * (TILE_WORDS + 4);
-constexpr uint32_t WS_PMR_OFF = (WS_PAT_OFF + PAT_WORDS + 3) & ~3u;
-constexpr size_t WS_SMEM = (size_t)WS_PMR_OFF * 4 + NWIN * 8;
+// k_verify_ws dynamic smem: [tile 0][tile 1] (wheel-6, TILE6_WORDS each)[patterns][masks6]
+constexpr uint32_t WS_PAT_OFF = 2 * TILE6_WORDS;
+constexpr uint32_t WS_MASK_OFF = (WS_PAT_OFF + PAT6_WORDS + 3) & ~3u;
+constexpr size_t WS_SMEM = (size_t)WS_MASK_OFF * 4 + 3 * NWIN6 * 8;
 
 // ---- launchers (gb_kernels.cu); all asynchronous on `st`
-cudaError_t launch_init_tables(uint32_t* pat, uint64_t* pmr, uint64_t p_small, cudaStream_t st);
+cudaError_t launch_init_tables(uint32_t* pat, uint64_t* pmr, uint32_t* pat6, uint64_t* masks6, uint64_t p_small,
+                               cudaStream_t st);
 cudaError_t launch_seed_primes(uint32_t lim, uint32_t* out, uint32_t* count, cudaStream_t st);
 cudaError_t launch_sieve_interval(uint64_t lo, uint64_t n_cells, const uint32_t* primes, uint32_t iA0,
                                   uint32_t iA1, uint32_t iB1, const uint32_t* pat, uint32_t* out,
@@ -84,6 +83,7 @@ cudaError_t launch_phase2_one(uint64_t n, uint64_t* out, cudaStream_t st);
 cudaError_t launch_is_prime_batch(const uint64_t* v, uint8_t* out, uint64_t n, cudaStream_t st);
 cudaError_t launch_smem_peak(uint32_t iters, uint32_t* sink, int grid, cudaStream_t st);
 int verify_occupancy(int* blocks_per_sm);
+int debug_stats(unsigned long long* out, int reset); // GB_STATS builds only (returns 2 otherwise)
 constexpr int SMEM_PEAK_THREADS = 512; // k_smem_peak: 2 CTAs x 512 threads per SM
 
 } // namespace gbk

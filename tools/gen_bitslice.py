@@ -85,6 +85,67 @@ def gen_scan(name, zmax, shf_every):
     return "\n".join(L), len(zs), nplanes, K
 
 
+def gen_scan6(name, r, pmax):
+    """Wheel-6 scan for the words of evens n = r (mod 6).  The tile holds
+    two arrays, A: q = Q + 6k (q = 1 mod 6) and B: q = Q + 4 + 6k (q = 5 mod 6);
+    lane bit i of word w is class-r even t = 32w - delta + i, whose candidate
+    p reads array cell k = t + G - g with g = (p - eps)/6 (A) or
+    (p + 4 - eps)/6 (B), eps = (r - 1) mod 6.  Only candidates with n - p
+    prime-capable (q = +-1 mod 6) exist for the class: r = 2 -> p = 3 (B) and
+    p = 1 mod 6 (A); r = 4 -> p = 3 (A) and p = 5 mod 6 (B); r = 0 -> p = 5
+    mod 6 (A) and p = 1 mod 6 (B).  a0..a2 / b0..b2 = array words WB-2..WB."""
+    eps = (r - 1) % 6
+    cands = []
+    for p in odd_primes(pmax):
+        if p == 3:
+            if r == 2:
+                cands.append((p, "b", (p + 4 - eps) // 6))
+            elif r == 4:
+                cands.append((p, "a", (p - eps) // 6))
+            continue
+        q = (r - p) % 6
+        if q == 1:
+            cands.append((p, "a", (p - eps) // 6))
+        elif q == 5:
+            cands.append((p, "b", (p + 4 - eps) // 6))
+    zs = [(p - 3) // 2 for p, _, _ in cands]
+    zmax = (pmax - 3) // 2
+    nplanes = zmax.bit_length()
+    L = []
+    L.append(f"// class r = {r}: {len(cands)} candidates p <= {pmax}; planes Z[0..{nplanes - 1}] of z = (p - 3)/2")
+    L.append(f"__device__ __forceinline__ void {name}(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t b0, uint32_t b1, "
+             f"uint32_t b2, uint32_t& U, uint32_t (&Z)[{nplanes}]) {{")
+    L.append("    uint32_t S;")
+    open_iv = {}
+    last_in_iv = {}
+    for b in range(nplanes):
+        for idx, z in enumerate(zs):
+            if (z >> b) & 1:
+                last_in_iv[(b, z >> b)] = idx
+    first_write = [True] * nplanes
+    for idx, ((p, arr, g), z) in enumerate(zip(cands, zs)):
+        for b in range(nplanes):
+            if (z >> b) & 1 and open_iv.get(b) != (z >> b):
+                open_iv[b] = z >> b
+                L.append(f"    const uint32_t s{b}_{z >> b} = U;")
+        k = (g + 31) // 32
+        sh = (-g) % 32
+        w = [f"{arr}0", f"{arr}1", f"{arr}2"]
+        src = w[2 - k] if sh == 0 else f"__funnelshift_r({w[2 - k]}, {w[3 - k]}, {sh})"
+        L.append(f"    S = {src}; // p = {p}")
+        L.append("    U &= ~S;")
+        for b in range(nplanes):
+            if (z >> b) & 1 and last_in_iv[(b, z >> b)] == idx:
+                op = "=" if first_write[b] else "|="
+                first_write[b] = False
+                L.append(f"    Z[{b}] {op} s{b}_{z >> b} & ~U;")
+    for b in range(nplanes):
+        if first_write[b]:
+            L.append(f"    Z[{b}] = 0u;")
+    L.append("}")
+    return "\n".join(L), len(cands), nplanes
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shf-every", type=int, default=1)
@@ -115,6 +176,13 @@ def main():
         parts.append(f"constexpr int {name.upper()}_WORDS = {K + 1};  // tile words t0..t{K}")
         parts.append(f"constexpr int {name.upper()}_PLANES = {npl};")
         parts.append(code)
+    parts.append("")
+    parts.append("// ---- wheel-6 layout (k_verify_ws): one scan per residue class of n mod 6")
+    for r in (0, 2, 4):
+        code, n, npl = gen_scan6(f"bs6_scan_r{r}", r, 257)
+        parts.append("")
+        parts.append(code)
+    parts.append("constexpr int BS6_PLANES = 7;")
     parts.append("")
     parts.append("} // namespace gbk")
     with open(OUT, "w") as f:

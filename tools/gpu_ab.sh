@@ -1,2 +1,3 @@
 bash tools/gpu_quick.sh
-LIMS="1e12 1e13" bash tools/gpu_variants.sh
+LIMS="${LIMS:-1e12 1e13}" bash tools/gpu_variants.sh
+if [ -n "$NCU" ]; then LIMS="1e12" bash tools/gpu_ncu.sh; fi

@@ -25,3 +25,10 @@ for rep in range(2):
     dt, segs, evens, sp, sh, mx = run()
     print(f"limit={limit:.0e} time={dt:.3f}s segs={segs} evens={evens} rate={evens/dt:.4e}/s sum={sp} hash={sh} max={mx}", flush=True)
 print("kernel times", dev.kernel_times(reset=True), "launches", dev.launch_count())
+try:
+    import ctypes as C
+    v = (C.c_uint64 * 8)()
+    if gb.lib().gb_debug_stats(v, 1) == 0:
+        print("stats [generic evens, inplace deep, queued deep, deep rounds, stragglers, fast blocks, generic blocks]:", list(v))
+except Exception as e:
+    print("no stats:", e)
