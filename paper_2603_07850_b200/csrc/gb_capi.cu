@@ -96,7 +96,8 @@ struct gb_dev {
     uint32_t* d_primes = nullptr;
     uint32_t iA0 = 0, iA1 = 0, iB1 = 0; // tile prime index ranges
     uint32_t iW1 = 0;                   // first tile prime >= W
-    uint16_t* d_wsplit = nullptr;       // [NWARPS][32] balanced warp-cooperative primes
+    uint16_t* d_wsplit = nullptr;       // [SPLIT_WARPS][32] balanced warp-cooperative primes
+    uint32_t sw = WS_SW_LIGHT;          // sieve warps of the fused kernel
     uint64_t* d_m64 = nullptr;          // floor(2^64 / p) per base prime
     uint64_t iL0 = 0, iL1 = 0;          // large primes
     uint32_t* d_pat = nullptr;
@@ -255,6 +256,7 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     A.iB1 = d->iB1;
     A.iW1 = d->iW1;
     A.np = np;
+    A.sw = d->sw;
     A.pmc = b.d_pmc;
     A.wsplit = d->d_wsplit;
     A.qg = large ? b.d_qg : nullptr;
@@ -519,12 +521,14 @@ static int build_tables(gb_dev* d) {
     {
         // warp-cooperative primes [iA0, iA1) to warps, longest first onto the
         // least loaded warp (cost ~ strikes per lane W / 32p + setup)
+        d->sw = (d->iB1 - d->iA0) > WS_HEAVY_PRIMES ? WS_SW_HEAVY : WS_SW_LIGHT;
+        const int nwarps = (int)d->sw;
         std::vector<uint16_t> ws(SPLIT_WARPS * 32, 0xFFFF);
-        std::vector<double> load(SPLIT_WARPS, 0.0);
-        std::vector<int> cnt(SPLIT_WARPS, 0);
+        std::vector<double> load(nwarps, 0.0);
+        std::vector<int> cnt(nwarps, 0);
         for (uint32_t i = d->iA0; i < d->iA1; ++i) { // ascending p = descending cost
             int best = -1;
-            for (int w = 0; w < SPLIT_WARPS; ++w)
+            for (int w = 0; w < nwarps; ++w)
                 if (cnt[w] < 32 && (best < 0 || load[w] < load[best])) best = w;
             if (best < 0) GB_FAIL(d, GB_ERR_INTERNAL, "too many warp-cooperative primes");
             ws[best * 32 + cnt[best]++] = (uint16_t)(i - d->iA0);

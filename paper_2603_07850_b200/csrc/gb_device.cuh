@@ -29,15 +29,20 @@ constexpr int THREADS = W_LOG2 >= 20 ? 1024 : 512; // threads per CTA of the fus
 constexpr int CTAS_PER_SM = W_LOG2 >= 20 ? 1 : 2;
 constexpr int NWARPS = THREADS / 32;
 // Warp-specialised fused kernel (k_verify_ws): one CTA of WS_THREADS per SM,
-// WS_ST sieve threads + WS_CT check threads.
-#ifndef GB_WS_SIEVE_WARPS
-#define GB_WS_SIEVE_WARPS 12
+// 32 SW sieve threads + the rest checking.  Two splits are compiled; the host
+// takes the heavy-sieve one when the block's tile primes exceed
+// WS_HEAVY_PRIMES (measured: 12 sieve warps best at 1e12, 16 at 1e13).
+#ifndef GB_WS_SW_LIGHT
+#define GB_WS_SW_LIGHT 12
+#endif
+#ifndef GB_WS_SW_HEAVY
+#define GB_WS_SW_HEAVY 16
 #endif
 constexpr int WS_THREADS = 1024;
-constexpr int WS_ST = 32 * GB_WS_SIEVE_WARPS;
-constexpr int WS_CT = WS_THREADS - WS_ST;
-// warps of the group that runs the warp-cooperative strikes
-constexpr int SPLIT_WARPS = WS_ST / 32;
+constexpr int WS_SW_LIGHT = GB_WS_SW_LIGHT, WS_SW_HEAVY = GB_WS_SW_HEAVY;
+constexpr uint32_t WS_HEAVY_PRIMES = 150000;
+// warps of the group that runs the warp-cooperative strikes (max of the splits)
+constexpr int SPLIT_WARPS = WS_SW_HEAVY > WS_SW_LIGHT ? WS_SW_HEAVY : WS_SW_LIGHT;
 constexpr uint32_t P_TILE_MAX = 1u << 22; // base primes above: K_large (global strikes)
 constexpr uint32_t P_WARP_MAX = 1024;     // primes below: warp-cooperative strikes
 constexpr uint32_t FIRST_STRIKE_P = 53;   // primes below are in the presieve patterns

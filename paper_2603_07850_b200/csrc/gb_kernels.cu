@@ -1146,31 +1146,32 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
 }
 
 // Warp-specialised fused kernel: one 1024-thread CTA per SM, two wheel-6
-// tile buffers.  The first WS_ST threads (the sieve group) sieve block k
-// into buffer k & 1 while the other WS_CT threads (the check group) check
+// tile buffers.  The first 32 SW threads (the sieve group) sieve block k
+// into buffer k & 1 while the other threads (the check group) check
 // block k - 1 in the other buffer.  Named barriers hand buffers over:
 // FULL[b] (sieve arrives, check waits) and EMPTY[b] (check arrives, sieve
 // waits), so the atomic-heavy sieve and the ALU-heavy check overlap instead
 // of alternating at CTA barriers.
 constexpr int BAR_S = 1, BAR_C = 2, BAR_FULL = 3, BAR_EMPTY = 5; // FULL/EMPTY + buffer
 
-template <bool PMIN>
+template <bool PMIN, int SW>
 __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
+    constexpr int ST = 32 * SW, CT = WS_THREADS - ST; // sieve / check threads
     extern __shared__ __align__(16) uint32_t smem[];
     uint32_t* tiles = smem;                                 // 2 x TILE6_WORDS
     uint32_t* pat6 = smem + WS_PAT_OFF;                     // PAT6_WORDS
     uint64_t* masks6 = (uint64_t*)(smem + WS_MASK_OFF);     // 3 x NWIN6
     __shared__ uint32_t s_fb[2];
-    __shared__ unsigned long long s_red[WS_CT / 32][3];
+    __shared__ unsigned long long s_red[CT / 32][3];
     __shared__ unsigned long long s_key;
-    __shared__ uint32_t s_q[WS_CT / 32][QCAP];
+    __shared__ uint32_t s_q[CT / 32][QCAP];
 
     for (uint32_t i = threadIdx.x; i < PAT6_WORDS; i += blockDim.x) pat6[i] = A.gpat6[i];
     for (uint32_t i = threadIdx.x; i < 3u * NWIN6; i += blockDim.x) masks6[i] = A.masks6[i];
     for (uint32_t i = threadIdx.x; i < 2 * TILE6_WORDS; i += blockDim.x) tiles[i] = 0; // pads stay zero
     __syncthreads();
     const int NB = WS_THREADS; // participants of FULL / EMPTY
-    if (threadIdx.x < WS_ST) {
+    if (threadIdx.x < ST) {
         // ---- sieve group
         const uint32_t tid = threadIdx.x;
         uint32_t fb_next = 0;
@@ -1180,7 +1181,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
             uint32_t* tile = tiles + bs * TILE6_WORDS;
             if (k >= 2) nb_sync(BAR_EMPTY + bs, NB); // check group done with block k - 2
             if (tid == 0) s_fb[bs] = fb_next;
-            gbar<WS_ST>(BAR_S);
+            gbar<ST>(BAR_S);
             const uint32_t fb = s_fb[bs];
             if (fb >= A.total_blocks) {
                 if (k >= 1) nb_sync(BAR_EMPTY + (bs ^ 1), NB); // absorb the last EMPTY
@@ -1190,13 +1191,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
             if (tid == 0) fb_next = atomicAdd(A.block_counter, 1u);
             const BlockInfo I = block_info(A, fb);
 #ifndef GB_SKIP_SIEVE // timing probe: check group alone (on stale tiles)
-            sieve_block<WS_ST>(A, tile, pat6, I, tid, BAR_S);
+            sieve_block<ST>(A, tile, pat6, I, tid, BAR_S);
 #endif
             nb_arrive(BAR_FULL + bs, NB);
         }
     } else {
         // ---- check group
-        const uint32_t tid = threadIdx.x - WS_ST;
+        const uint32_t tid = threadIdx.x - ST;
         for (uint32_t k = 0;; ++k) {
             const uint32_t bs = k & 1;
             nb_sync(BAR_FULL + bs, NB);
@@ -1204,7 +1205,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
             if (fb >= A.total_blocks) return;
             const BlockInfo I = block_info(A, fb);
 #ifndef GB_SKIP_CHECK // timing probe: sieve group alone
-            check_block<PMIN, WS_CT>(A, tiles + bs * TILE6_WORDS, masks6, I, tid, BAR_C, s_red, &s_key, s_q);
+            check_block<PMIN, CT>(A, tiles + bs * TILE6_WORDS, masks6, I, tid, BAR_C, s_red, &s_key, s_q);
 #endif
             nb_arrive(BAR_EMPTY + bs, NB);
         }
@@ -1461,10 +1462,15 @@ cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint3
     return cudaGetLastError();
 }
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st) {
-    if (a.pmin_out)
-        k_verify_ws<true><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
-    else
-        k_verify_ws<false><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
+    // the sieve/check split follows the sieve's share of the work, which
+    // grows with the number of tile primes (a.sw, chosen by the host)
+    if (a.sw == WS_SW_HEAVY) {
+        if (a.pmin_out) k_verify_ws<true, WS_SW_HEAVY><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
+        else k_verify_ws<false, WS_SW_HEAVY><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
+    } else {
+        if (a.pmin_out) k_verify_ws<true, WS_SW_LIGHT><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
+        else k_verify_ws<false, WS_SW_LIGHT><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
+    }
     return cudaGetLastError();
 }
 cudaError_t launch_stragglers(const SegJob* jobs, const StragEntry* list, const unsigned int* list_count,
@@ -1494,14 +1500,23 @@ int verify_occupancy(int* blocks_per_sm) {
     if (cudaFuncSetAttribute(k_sieve_interval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SIEVE_SMEM) !=
         cudaSuccess)
         return 1;
-    if (cudaFuncSetAttribute(k_verify_ws<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_SMEM) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(k_verify_ws<false, WS_SW_LIGHT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)WS_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(k_verify_ws<true, WS_SW_LIGHT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)WS_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(k_verify_ws<false, WS_SW_HEAVY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)WS_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(k_verify_ws<true, WS_SW_HEAVY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)WS_SMEM) != cudaSuccess)
         return 1;
-    if (cudaFuncSetAttribute(k_verify_ws<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_SMEM) !=
-        cudaSuccess)
+    int o1 = 0, o2 = 0;
+    if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o1, k_verify_ws<false, WS_SW_LIGHT>, WS_THREADS, WS_SMEM) !=
+            cudaSuccess ||
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&o2, k_verify_ws<false, WS_SW_HEAVY>, WS_THREADS, WS_SMEM) !=
+            cudaSuccess)
         return 1;
-    return (int)cudaOccupancyMaxActiveBlocksPerMultiprocessor(blocks_per_sm, k_verify_ws<false>, WS_THREADS,
-                                                              WS_SMEM);
+    *blocks_per_sm = o1 < o2 ? o1 : o2;
+    return 0;
 }
 
 } // namespace gbk

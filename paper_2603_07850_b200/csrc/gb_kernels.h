@@ -31,6 +31,7 @@ struct VerifyArgs {
     uint32_t iA0, iA1, iB1;       // tile prime index ranges
     uint32_t iW1;                 // first tile prime >= M6 (strikes an array at most once)
     uint32_t np;                  // pmc row length (iB1 - iA0)
+    uint32_t sw;                  // sieve warps of the kernel split (WS_SW_LIGHT / WS_SW_HEAVY)
     const uint4* pmc;             // nslots * np {p, floor(2^32/p), p - 1 - k0, 4 6^-1 mod p}
     const uint16_t* wsplit;       // [SPLIT_WARPS][32] warp-cooperative row indices (0xFFFF = none)
     const uint32_t* qg;           // large-prime wheel-6 bitmask (nullptr = none)
