@@ -422,7 +422,8 @@ def main():
             "paper_note": {10**12: "1x RTX 5090 (PAPER.md:454)",
                            10**13: "4x RTX 5090 (PAPER.md:455)"}.get(args.limit),
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
-                    "d2h_bytes_per_step": d2h, "seconds_per_step": sum(e2e_s) / args.steps},
+                    "d2h_bytes_per_step": d2h, "seconds_per_step": sum(e2e_s) / args.steps,
+                    "step_seconds": e2e_s},
             "gpu_launches": launches,
             "roofline": roofline,
             "cpu_baseline": ({k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}
