@@ -633,10 +633,12 @@ struct K3Acc {
     }
 };
 
-// Candidates p <= 257 are scanned bit-sliced (gb_bitslice.cuh bs6_scan_r*),
+// Candidates p <= PBS are scanned bit-sliced (gb_bitslice.cuh bs6_scan_r*),
 // 32 class-r evens per lane; the few evens left ("deep") continue per even
-// over 64-wide windows of g = p div 6.
-constexpr uint32_t PBS = 257;
+// over 64-wide windows of g = p div 6, from the first window with an
+// unscanned candidate.
+constexpr uint32_t PBS = BS6_PMAX;
+constexpr uint32_t DEEP_J0 = ((PBS + 1) / 6) / 64;
 constexpr int NPL = BS6_PLANES;          // z planes
 constexpr uint32_t QCAP = 512;           // per-warp deep-even queue (classes 2, 4 run ~2x the mean deep rate)
 
@@ -704,7 +706,8 @@ __device__ __forceinline__ void deep_even6(const uint32_t* tile, const uint64_t*
                                            const VerifyArgs& A, uint32_t jlim_small, K3Acc& acc) {
     GB_STAT(1, 1);
     uint32_t p = 0;
-    for (uint32_t j = 0; j < (uint32_t)NWIN6 && !p; ++j) p = window_hit6(tile, masks6, C.r, C.G, t, j, ~0ull, ~0ull, ~0ull);
+    for (uint32_t j = DEEP_J0; j < (uint32_t)NWIN6 && !p; ++j)
+        p = window_hit6(tile, masks6, C.r, C.G, t, j, ~0ull, ~0ull, ~0ull);
     const uint32_t il = ci + 3 * t;
     if (p) acc.add(p, il);
     else push_straggler(A, J, s, i0 + il, jlim_small, 0);
@@ -830,12 +833,14 @@ __device__ __forceinline__ uint32_t vsum_by_index(uint32_t (&V)[VPL], uint32_t (
 // U out = those with no candidate p <= PBS; Z = planes of the found z.
 __device__ __forceinline__ void scan_word6(const uint32_t* tile, uint32_t r, uint32_t WB, uint32_t& U,
                                            uint32_t (&Z)[NPL]) {
+    static_assert(BS6_WORDS == 4, "scan_word6 loads WB-3 .. WB of each array");
     const uint32_t* a = arr_a(tile) + WB;
     const uint32_t* b = arr_b(tile) + WB;
-    const uint32_t a0 = a[-2], a1 = a[-1], a2 = a[0], b0 = b[-2], b1 = b[-1], b2 = b[0];
-    if (r == 0) bs6_scan_r0(a0, a1, a2, b0, b1, b2, U, Z);
-    else if (r == 2) bs6_scan_r2(a0, a1, a2, b0, b1, b2, U, Z);
-    else bs6_scan_r4(a0, a1, a2, b0, b1, b2, U, Z);
+    const uint32_t a0 = a[-3], a1 = a[-2], a2 = a[-1], a3 = a[0];
+    const uint32_t b0 = b[-3], b1 = b[-2], b2 = b[-1], b3 = b[0];
+    if (r == 0) bs6_scan_r0(a0, a1, a2, a3, b0, b1, b2, b3, U, Z);
+    else if (r == 2) bs6_scan_r2(a0, a1, a2, a3, b0, b1, b2, b3, U, Z);
+    else bs6_scan_r4(a0, a1, a2, a3, b0, b1, b2, b3, U, Z);
 }
 
 // Valid bits of word w of a class with T evens and alignment delta.
@@ -1042,7 +1047,7 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
                         while (U[k]) {
                             const uint32_t bit = __ffs(U[k]) - 1;
                             U[k] &= U[k] - 1;
-                            q[pos++] = (32 * w - delta + bit) | (ci << 18);
+                            q[pos++] = (32 * w - delta + bit) | (ci << 18) | (DEEP_J0 << 20);
                         }
                     }
                     qn += total;

@@ -85,6 +85,12 @@ def gen_scan(name, zmax, shf_every):
     return "\n".join(L), len(zs), nplanes, K
 
 
+def scan6_words(pmax):
+    """tile words per array every class scan reads (the largest g over classes)"""
+    gmax = max((p + 1) // 6 for p in odd_primes(pmax))
+    return gmax // 32 + 2
+
+
 def gen_scan6(name, r, pmax):
     """Wheel-6 scan for the words of evens n = r (mod 6).  The tile holds
     two arrays, A: q = Q + 6k (q = 1 mod 6) and B: q = Q + 4 + 6k (q = 5 mod 6);
@@ -113,8 +119,9 @@ def gen_scan6(name, r, pmax):
     nplanes = zmax.bit_length()
     L = []
     L.append(f"// class r = {r}: {len(cands)} candidates p <= {pmax}; planes Z[0..{nplanes - 1}] of z = (p - 3)/2")
-    L.append(f"__device__ __forceinline__ void {name}(uint32_t a0, uint32_t a1, uint32_t a2, uint32_t b0, uint32_t b1, "
-             f"uint32_t b2, uint32_t& U, uint32_t (&Z)[{nplanes}]) {{")
+    nw = scan6_words(pmax)  # words per array: WB-(nw-1) .. WB
+    args = ", ".join([f"uint32_t a{k}" for k in range(nw)] + [f"uint32_t b{k}" for k in range(nw)])
+    L.append(f"__device__ __forceinline__ void {name}({args}, uint32_t& U, uint32_t (&Z)[{nplanes}]) {{")
     L.append("    uint32_t S;")
     open_iv = {}
     last_in_iv = {}
@@ -130,8 +137,9 @@ def gen_scan6(name, r, pmax):
                 L.append(f"    const uint32_t s{b}_{z >> b} = U;")
         k = (g + 31) // 32
         sh = (-g) % 32
-        w = [f"{arr}0", f"{arr}1", f"{arr}2"]
-        src = w[2 - k] if sh == 0 else f"__funnelshift_r({w[2 - k]}, {w[3 - k]}, {sh})"
+        w = [f"{arr}{i}" for i in range(nw)]  # w[nw-1] = word WB
+        top = nw - 1
+        src = w[top - k] if sh == 0 else f"__funnelshift_r({w[top - k]}, {w[top - k + 1]}, {sh})"
         L.append(f"    S = {src}; // p = {p}")
         L.append("    U &= ~S;")
         for b in range(nplanes):
@@ -143,12 +151,13 @@ def gen_scan6(name, r, pmax):
         if first_write[b]:
             L.append(f"    Z[{b}] = 0u;")
     L.append("}")
-    return "\n".join(L), len(cands), nplanes
+    return "\n".join(L), len(cands), nplanes, nw
 
 
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shf-every", type=int, default=1)
+    ap.add_argument("--pbs6", type=int, default=385, help="largest bit-sliced candidate (wheel-6 scans)")
     args = ap.parse_args()
     parts = []
     parts.append(f"// gb_bitslice.cuh -- GENERATED by tools/gen_bitslice.py --shf-every {args.shf_every}; do not edit.")
@@ -162,27 +171,14 @@ def main():
     parts.append("")
     parts.append("namespace gbk {")
     parts.append("")
-    parts.append("// 2^k; in constant memory so the IMAD funnel below is not folded into SHF")
-    parts.append("__constant__ uint32_t c_pow2[32] = {" + ", ".join(f"{1 << k}u" for k in range(32)) + "};")
-    parts.append("")
-    parts.append("// funnel shift right of (hi:lo) by sh (0 < sh < 32) on the FMA pipe")
-    parts.append("__device__ __forceinline__ uint32_t fsr_fma(uint32_t lo, uint32_t hi, int sh) {")
-    parts.append("    const uint32_t K = c_pow2[32 - sh];")
-    parts.append("    return hi * K + __umulhi(lo, K);")
-    parts.append("}")
-    for name, zmax in (("bs_scan64", 63), ("bs_scan128", 127)):
-        code, n, npl, K = gen_scan(name, zmax, args.shf_every)
-        parts.append("")
-        parts.append(f"constexpr int {name.upper()}_WORDS = {K + 1};  // tile words t0..t{K}")
-        parts.append(f"constexpr int {name.upper()}_PLANES = {npl};")
-        parts.append(code)
-    parts.append("")
     parts.append("// ---- wheel-6 layout (k_verify_ws): one scan per residue class of n mod 6")
     for r in (0, 2, 4):
-        code, n, npl = gen_scan6(f"bs6_scan_r{r}", r, 257)
+        code, n, npl, nw = gen_scan6(f"bs6_scan_r{r}", r, args.pbs6)
         parts.append("")
         parts.append(code)
-    parts.append("constexpr int BS6_PLANES = 7;")
+    parts.append(f"constexpr uint32_t BS6_PMAX = {args.pbs6};   // candidates p <= BS6_PMAX are bit-sliced")
+    parts.append(f"constexpr int BS6_PLANES = {npl};")
+    parts.append(f"constexpr int BS6_WORDS = {nw};    // tile words per array a scan reads (WB-{nw - 1} .. WB)")
     parts.append("")
     parts.append("} // namespace gbk")
     with open(OUT, "w") as f:
