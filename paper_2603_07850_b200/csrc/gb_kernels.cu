@@ -806,11 +806,10 @@ __device__ __forceinline__ uint32_t idx_sum(uint32_t x) {
            8 * __popc(x & 0xFF00FF00u) + 16 * __popc(x & 0xFFFF0000u);
 }
 
-// Deferred sum p * (bit index) of VACC words: V = bit-sliced per-position
+// Deferred sum p * (bit index) of VFLUSH words: V = bit-sliced per-position
 // sums of z (VPL planes), FC = per-position found counts (FPL planes);
 // p = 3 + 2z, so the sum is 2 sum_b 2^b idx(V_b) + 3 sum_k 2^k idx(FC_k).
 // Resets V and FC.
-constexpr uint32_t VACC = 4;  // words per compaction batch
 constexpr uint32_t VFLUSH = 4; // words per vertical-counter reduction
 constexpr int VPL = NPL + 2;   // 4 * 127 < 2^9
 constexpr int FPL = 3;         // 4 < 2^3
@@ -948,7 +947,7 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
         uint32_t* q = s_q[warp];
         uint32_t qn = 0;   // warp-uniform queue length (< 32 between batches)
         uint32_t sp32 = 0; // sum p of the bit-sliced evens (< 2^32 per lane)
-        // sum p * (bit index) is deferred: z planes and found bits of VACC
+        // sum p * (bit index) is deferred: z planes and found bits of VFLUSH
         // words are summed per bit position as bit-sliced counters V (z) and
         // FC (found), then reduced by bit index once
         uint32_t V[VPL], FC[FPL];
@@ -963,107 +962,88 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
             const uint32_t T = ne > ci ? (ne - ci + 2) / 3 : 0;
             const uint32_t delta = C.G & 31;
             const uint32_t nw = (T + delta + 31) >> 5;
-            for (uint32_t wb = warp * 32; wb < nw; wb += VACC * GT) {
-                // the scan is not unrolled over the VACC words (code size:
-                // the three class scans must stay in the instruction cache);
-                // the words' leftovers go to named registers by select
-                uint32_t U[VACC];
+            // one word (32 class-ci evens) per lane per step; the scan is not
+            // unrolled (code size: the three class scans must stay in the
+            // instruction cache)
+            for (uint32_t wb = warp * 32; wb < nw; wb += GT) {
+                const uint32_t w = wb + lane;
+                uint32_t U = 0;
+                if (w < nw) {
+                    const uint32_t valid = (w == 0 || w + 1 == nw) ? word_mask6(w, T, delta) : ~0u;
+                    uint32_t Z[NPL];
+                    U = valid;
+                    scan_word6(tile, C.r, w + (C.G >> 5), U, Z);
+                    const uint32_t F = valid & ~U;
+                    // p = 3 + 2z: sum p of the word; il = ci + 3 (32w - delta + i)
+                    uint32_t P = 3 * __popc(F);
 #pragma unroll
-                for (uint32_t k = 0; k < VACC; ++k) U[k] = 0;
-#pragma unroll 1
-                for (uint32_t k = 0; k < VACC; ++k) {
-                    const uint32_t w = wb + k * GT + lane;
-                    uint32_t Uk = 0;
-                    if (w < nw) {
-                        const uint32_t valid = (w == 0 || w + 1 == nw) ? word_mask6(w, T, delta) : ~0u;
-                        uint32_t Z[NPL];
-                        Uk = valid;
-                        scan_word6(tile, C.r, w + (C.G >> 5), Uk, Z);
-                        const uint32_t F = valid & ~Uk;
-                        // p = 3 + 2z: sum p of the word; il = ci + 3 (32w - delta + i)
-                        uint32_t P = 3 * __popc(F);
+                    for (int bp = 0; bp < NPL; ++bp) P += (2u << bp) * __popc(Z[bp]);
+                    sp32 += P;
+                    acc.spi += (uint64_t)P * (uint64_t)((int64_t)ci + 96 * (int64_t)w - 3 * (int64_t)delta);
+                    // V += Z, FC += F (ripple-carry, bit-sliced)
+                    uint32_t cy = V[0] & Z[0];
+                    V[0] ^= Z[0];
 #pragma unroll
-                        for (int bp = 0; bp < NPL; ++bp) P += (2u << bp) * __popc(Z[bp]);
-                        sp32 += P;
-                        acc.spi += (uint64_t)P * (uint64_t)((int64_t)ci + 96 * (int64_t)w - 3 * (int64_t)delta);
-                        // V += Z, FC += F (ripple-carry, bit-sliced)
-                        uint32_t cy = V[0] & Z[0];
-                        V[0] ^= Z[0];
-#pragma unroll
-                        for (int bp = 1; bp < NPL; ++bp) {
-                            const uint32_t v = V[bp], z = Z[bp];
-                            V[bp] = v ^ z ^ cy;
-                            cy = (v & z) | (cy & (v ^ z));
-                        }
-#pragma unroll
-                        for (int bp = NPL; bp < VPL; ++bp) {
-                            const uint32_t v = V[bp];
-                            V[bp] = v ^ cy;
-                            cy = v & cy;
-                        }
-                        cy = F;
-#pragma unroll
-                        for (int kk = 0; kk < FPL; ++kk) {
-                            const uint32_t f = FC[kk];
-                            FC[kk] = f ^ cy;
-                            cy = f & cy;
-                        }
-                        if constexpr (PMIN) {
-                            for (uint32_t i = 0; i < 32; ++i) {
-                                if (!((F >> i) & 1)) continue;
-                                uint32_t z = 0;
-#pragma unroll
-                                for (int bp = 0; bp < NPL; ++bp) z |= ((Z[bp] >> i) & 1) << bp;
-                                A.pmin_out[i0 + ci + 3 * (32 * w - delta + i)] = 3 + 2 * z;
-                            }
-                        }
+                    for (int bp = 1; bp < NPL; ++bp) {
+                        const uint32_t v = V[bp], z = Z[bp];
+                        V[bp] = v ^ z ^ cy;
+                        cy = (v & z) | (cy & (v ^ z));
                     }
 #pragma unroll
-                    for (uint32_t kk = 0; kk < VACC; ++kk)
-                        if (kk == k) U[kk] = Uk;
+                    for (int bp = NPL; bp < VPL; ++bp) {
+                        const uint32_t v = V[bp];
+                        V[bp] = v ^ cy;
+                        cy = v & cy;
+                    }
+                    cy = F;
+#pragma unroll
+                    for (int kk = 0; kk < FPL; ++kk) {
+                        const uint32_t f = FC[kk];
+                        FC[kk] = f ^ cy;
+                        cy = f & cy;
+                    }
+                    if constexpr (PMIN) {
+                        for (uint32_t i = 0; i < 32; ++i) {
+                            if (!((F >> i) & 1)) continue;
+                            uint32_t z = 0;
+#pragma unroll
+                            for (int bp = 0; bp < NPL; ++bp) z |= ((Z[bp] >> i) & 1) << bp;
+                            A.pmin_out[i0 + ci + 3 * (32 * w - delta + i)] = 3 + 2 * z;
+                        }
+                    }
                 }
-                if (++nbatch == VFLUSH / VACC) { // counters hold VFLUSH words
+                if (++nbatch == VFLUSH) { // counters hold VFLUSH words
                     acc.spi += 3ull * vsum_by_index(V, FC);
                     nbatch = 0;
                 }
-                // deep evens of the VACC words: compact into the warp queue with
-                // one warp prefix sum, drain 32 at a time
-                uint32_t cnt = 0;
-#pragma unroll
-                for (uint32_t k = 0; k < VACC; ++k) cnt += __popc(U[k]);
-                uint32_t incl = cnt;
-#pragma unroll
-                for (int o = 1; o < 32; o <<= 1) {
-                    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
-                    if (lane >= (uint32_t)o) incl += y;
-                }
-                const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+                // deep evens of the word: exclusive prefix of the lanes' counts
+                // by ballot per count threshold (counts are 0..2 almost always)
+                const uint32_t cnt = __popc(U);
+                const uint32_t cmax = __reduce_max_sync(0xffffffffu, cnt);
+                if (cmax == 0) continue;
+                const uint32_t total = __reduce_add_sync(0xffffffffu, cnt);
+                const uint32_t lt = (1u << lane) - 1;
+                uint32_t pre = 0;
+                for (uint32_t th = 1; th <= cmax; ++th) pre += __popc(__ballot_sync(0xffffffffu, cnt >= th) & lt);
                 if (lane == 0) GB_STAT(2, total);
                 if (qn + total <= QCAP) {
-                    uint32_t pos = qn + incl - cnt;
-#pragma unroll
-                    for (uint32_t k = 0; k < VACC; ++k) {
-                        const uint32_t w = wb + k * GT + lane;
-                        while (U[k]) {
-                            const uint32_t bit = __ffs(U[k]) - 1;
-                            U[k] &= U[k] - 1;
-                            q[pos++] = (32 * w - delta + bit) | (ci << 18) | (DEEP_J0 << 20);
-                        }
+                    uint32_t pos = qn + pre;
+                    const uint32_t t0 = 32 * w - delta; // wraps for w = 0; t0 + bit >= 0 for valid bits
+                    const uint32_t hi = (ci << 18) | (DEEP_J0 << 20);
+                    while (U) {
+                        const uint32_t bit = __ffs(U) - 1;
+                        U &= U - 1;
+                        q[pos++] = (t0 + bit) | hi;
                     }
                     qn += total;
                     __syncwarp();
                     while (qn >= 32)
                         qn = deep_round6<PMIN>(tile, masks6, q, qn, 32, lane, i0, s, J, CL, A, jlim_small, acc);
                 } else {
-#pragma unroll
-                    for (uint32_t k = 0; k < VACC; ++k) { // queue full: this lane's deep evens in place
-                        const uint32_t w = wb + k * GT + lane;
-                        while (U[k]) {
-                            const uint32_t bit = __ffs(U[k]) - 1;
-                            U[k] &= U[k] - 1;
-                            deep_even6<PMIN>(tile, masks6, 32 * w - delta + bit, CL[ci], ci, i0, s, J, A, jlim_small,
-                                             acc);
-                        }
+                    while (U) { // queue full: this lane's deep evens in place
+                        const uint32_t bit = __ffs(U) - 1;
+                        U &= U - 1;
+                        deep_even6<PMIN>(tile, masks6, 32 * w - delta + bit, CL[ci], ci, i0, s, J, A, jlim_small, acc);
                     }
                     __syncwarp();
                 }
