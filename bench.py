@@ -138,18 +138,34 @@ class Dist:
         if self.world != n_gpus and self.world > 1:
             raise SystemExit(f"--gpus {n_gpus} but WORLD_SIZE={self.world}")
         self.tdev = None
+        # GB_BENCH_BACKEND=gloo + GB_BENCH_SHARE_GPU=1: a box with fewer GPUs
+        # than ranks runs the multi-rank path (shared cursor, all-gather
+        # merge, max-over-ranks timing) with every rank on GPU 0 -- a
+        # correctness check of that path, not a scaling measurement
+        self.backend = os.environ.get("GB_BENCH_BACKEND", "nccl")
+        self.gpu = self.local_rank
+        if os.environ.get("GB_BENCH_SHARE_GPU") == "1":
+            import torch
+            self.gpu = self.local_rank % max(torch.cuda.device_count(), 1)
         if self.world > 1:
             import torch
             import torch.distributed as dist
-            torch.cuda.set_device(self.local_rank)
-            dist.init_process_group("nccl", device_id=torch.device("cuda", self.local_rank))
-            self.tdev = torch.device("cuda", self.local_rank)
+            torch.cuda.set_device(self.gpu)
+            if self.backend == "nccl":
+                dist.init_process_group("nccl", device_id=torch.device("cuda", self.gpu))
+                self.tdev = torch.device("cuda", self.gpu)
+            else:
+                dist.init_process_group(self.backend)
+                self.tdev = torch.device("cpu")
         self.tag = os.environ.get("MASTER_PORT", "0")
 
     def barrier(self):
         if self.world > 1:
             import torch.distributed as dist
-            dist.barrier(device_ids=[self.local_rank])
+            if self.backend == "nccl":
+                dist.barrier(device_ids=[self.gpu])
+            else:
+                dist.barrier()
 
     def max(self, x):
         if self.world == 1:
@@ -310,7 +326,7 @@ def main():
 
     import paper_2603_07850_b200 as gb
 
-    dev = gb.Device(args.limit, p_small=args.p_small, device=D.local_rank,
+    dev = gb.Device(args.limit, p_small=args.p_small, device=D.gpu,
                     max_seg_evens=args.seg_size)
     total_evens = (args.limit - args.start) // 2 + 1
 
@@ -336,7 +352,7 @@ def main():
     l0 = dev.launch_count()
     dev.kernel_times(reset=True)
     step_ms, merged = [], None
-    with ClockSampler(D.local_rank) as clk:
+    with ClockSampler(D.gpu) as clk:
         for k in range(args.steps):
             dev.flush_l2()
             dev.set_timing(1)
@@ -383,22 +399,26 @@ def main():
         "ncu_profile": prof_w.get("source"),
     }
 
-    # ---- e2e through the public API, host <-> device copies included
+    # ---- e2e through the public API, host <-> device copies included (one
+    # untimed pass first: a second handle's first open allocates its pinned
+    # and device buffers, later opens reuse them from the process arena)
     e2e_s, h2d, d2h = [], 0, 0
-    for k in range(args.steps):
+    for k in range(-1, args.steps):
         D.barrier()
         t0 = time.perf_counter()
         pool = make_pool(gb, D, args, f"e{k}")
-        with gb.Device(args.limit, p_small=args.p_small, device=D.local_rank,
+        with gb.Device(args.limit, p_small=args.p_small, device=D.gpu,
                        max_seg_evens=args.seg_size) as d2:
             r = gb.drain_pool(d2, pool).as_dict()
             hb, db = d2.io_bytes()
         release_pool(D, pool)
         m = D.merge(r)
-        e2e_s.append(D.max(time.perf_counter() - t0))
+        dt = D.max(time.perf_counter() - t0)
         if m != merged:
             raise SystemExit(f"e2e result differs from the device-timed pass: {m} vs {merged}")
         h2d, d2h = D.sum(hb), D.sum(db)
+        if k >= 0:
+            e2e_s.append(dt)
     e2e_value = args.steps * total_evens / sum(e2e_s)
 
     cpu = None
