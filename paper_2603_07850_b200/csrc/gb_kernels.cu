@@ -353,6 +353,13 @@ __device__ __forceinline__ uint64_t mod_magic(uint64_t x, uint64_t p, uint64_t m
     return r >= p ? r - p : r;
 }
 
+// 4 6^-1 mod p (array B's first index is A's minus this), without a division
+__device__ __forceinline__ uint32_t b_shift6(uint32_t p) {
+    uint64_t c = 4ull * inv6_mod(p); // < 4p
+    while (c >= p) c -= p;
+    return (uint32_t)c;
+}
+
 // First index k >= 0 of array A (q = Q + 6k) with p | q: (-Q) 6^-1 mod p.
 __device__ __forceinline__ uint32_t first_a6(const SegJob& J, uint32_t p, uint64_t m64) {
     uint64_t r = mod_magic(J.qbase, p, m64); // |Q| mod p
@@ -368,36 +375,35 @@ __device__ __forceinline__ uint32_t first_a6(const SegJob& J, uint32_t p, uint64
 __global__ void k_segment_offsets(const SegJob* __restrict__ jobs, uint32_t nslots,
                                   const uint32_t* __restrict__ primes, const uint64_t* __restrict__ m64,
                                   uint32_t iA0, uint32_t np, uint4* __restrict__ pmc) {
-    uint64_t total = (uint64_t)nslots * np;
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
-         t += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t s = (uint32_t)(t / np), i = (uint32_t)(t % np);
+    // grid: x over primes, y = slot (no 64-bit index division)
+    const uint32_t s = blockIdx.y;
+    const SegJob& J = jobs[s];
+    for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
         const uint32_t p = primes[iA0 + i];
-        const uint32_t k0 = first_a6(jobs[s], p, m64[iA0 + i]);
-        pmc[t] = make_uint4(p, (uint32_t)((1ull << 32) / p), p - 1 - k0, (uint32_t)((4ull * inv6_mod(p)) % p));
+        const uint32_t k0 = first_a6(J, p, m64[iA0 + i]);
+        pmc[(size_t)s * np + i] = make_uint4(p, (uint32_t)((1ull << 32) / p), p - 1 - k0, b_shift6(p));
     }
 }
 
 // Primes above P_TILE_MAX: strike the slot's global wheel-6 bitmask (array A
 // then array B, qg_words words each, cells relative to the slot's origin)
-// with RED.AND; the fused kernel ANDs the words into its tiles.
+// with RED.AND; the fused kernel ANDs the words into its tiles.  Grid: x over
+// primes, y = slot.
 __global__ void k_large_strike(const SegJob* __restrict__ jobs, uint32_t nslots,
                                const uint32_t* __restrict__ primes, const uint64_t* __restrict__ m64,
                                uint64_t iL0, uint64_t iL1, uint32_t* __restrict__ qg, uint64_t qg_stride_words) {
-    uint64_t np = iL1 - iL0;
-    uint64_t total = np * nslots;
-    for (uint64_t t = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; t < total;
-         t += (uint64_t)gridDim.x * blockDim.x) {
-        uint32_t s = (uint32_t)(t / np);
-        uint64_t i = iL0 + t % np;
-        const SegJob& j = jobs[s];
-        const uint64_t ncells = (uint64_t)j.qg_words * 32;
+    const uint32_t s = blockIdx.y;
+    const SegJob& j = jobs[s];
+    const uint32_t ncells = j.qg_words * 32;
+    uint32_t* ga = qg + s * qg_stride_words;
+    uint32_t* gb = ga + j.qg_words;
+    for (uint64_t i = iL0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < iL1;
+         i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t p = primes[i];
         const uint32_t k0 = first_a6(j, p, m64[i]);
-        const uint32_t c = (uint32_t)((4ull * inv6_mod(p)) % p);
+        const uint32_t c = b_shift6(p);
         const uint32_t k0b = k0 >= c ? k0 - c : k0 + p - c;
-        uint32_t* ga = qg + s * qg_stride_words;
-        uint32_t* gb = ga + j.qg_words;
+        // k + p can pass 2^32 (p < 2^32 near the 2^64 ceiling): 64-bit steps
         for (uint64_t k = k0; k < ncells; k += p) atomicAnd(&ga[k >> 5], ~(1u << (k & 31)));
         for (uint64_t k = k0b; k < ncells; k += p) atomicAnd(&gb[k >> 5], ~(1u << (k & 31)));
     }
@@ -902,8 +908,10 @@ __device__ __forceinline__ void sieve_block(const VerifyArgs& A, uint32_t* tile,
     presieve6(arr_a(tile), pat6, pha, tid, GT);
     presieve6(arr_b(tile), pat6, phb, tid, GT);
     gbar<GT>(bar);
+#ifndef GB_SKIP_STRIKES // timing probe: the check group on presieved-only tiles
     strike_verify6<GT>(tile, A.pmc + (size_t)I.s * A.np, A.iA1 - A.iA0, A.iW1 - A.iA0, A.iB1 - A.iA0, I.KB, tid,
                        A.wsplit);
+#endif
     if (A.qg != nullptr && I.J.qg_words) {
         gbar<GT>(bar);
         const uint32_t* ga = A.qg + I.s * A.qg_stride_words + I.KB / 32;
@@ -1175,9 +1183,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
             }
             if (tid == 0) fb_next = atomicAdd(A.block_counter, 1u);
             const BlockInfo I = block_info(A, fb);
-#ifndef GB_SKIP_SIEVE // timing probe: check group alone (on stale tiles)
             sieve_block<ST>(A, tile, pat6, I, tid, BAR_S);
-#endif
             nb_arrive(BAR_FULL + bs, NB);
         }
     } else {
@@ -1432,18 +1438,17 @@ cudaError_t launch_prime_magic64(const uint32_t* primes, uint64_t n, uint64_t* m
 }
 cudaError_t launch_segment_offsets(const SegJob* jobs, uint32_t nslots, const uint32_t* primes,
                                    const uint64_t* m64, uint32_t iA0, uint32_t np, uint4* pmc, cudaStream_t st) {
-    uint64_t total = (uint64_t)nslots * np;
-    if (!total) return cudaSuccess;
-    unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 16);
-    k_segment_offsets<<<grid, 256, 0, st>>>(jobs, nslots, primes, m64, iA0, np, pmc);
+    if (!np || !nslots) return cudaSuccess;
+    const unsigned gx = (unsigned)std::min<uint64_t>((np + 255) / 256, 148ull * 4);
+    k_segment_offsets<<<dim3(gx, nslots), 256, 0, st>>>(jobs, nslots, primes, m64, iA0, np, pmc);
     return cudaGetLastError();
 }
 cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, const uint64_t* m64,
                                 uint64_t iL0, uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, cudaStream_t st) {
-    uint64_t total = (uint64_t)nslots * (iL1 - iL0);
-    if (!total) return cudaSuccess;
-    unsigned grid = (unsigned)std::min<uint64_t>((total + 255) / 256, 148ull * 32);
-    k_large_strike<<<grid, 256, 0, st>>>(jobs, nslots, primes, m64, iL0, iL1, qg, qg_stride_words);
+    const uint64_t np = iL1 - iL0;
+    if (!np || !nslots) return cudaSuccess;
+    const unsigned gx = (unsigned)std::min<uint64_t>((np + 255) / 256, 148ull * 32 / nslots + 1);
+    k_large_strike<<<dim3(gx, nslots), 256, 0, st>>>(jobs, nslots, primes, m64, iL0, iL1, qg, qg_stride_words);
     return cudaGetLastError();
 }
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st) {
