@@ -38,7 +38,10 @@ constexpr int NWARPS = THREADS / 32;
 #ifndef GB_WS_SW_HEAVY
 #define GB_WS_SW_HEAVY 16
 #endif
-constexpr int WS_THREADS = 1024;
+#ifndef GB_WS_THREADS
+#define GB_WS_THREADS 1024
+#endif
+constexpr int WS_THREADS = GB_WS_THREADS;
 constexpr int WS_SW_LIGHT = GB_WS_SW_LIGHT, WS_SW_HEAVY = GB_WS_SW_HEAVY;
 constexpr uint32_t WS_HEAVY_PRIMES = 150000;
 // warps of the group that runs the warp-cooperative strikes (max of the splits)

@@ -668,20 +668,15 @@ struct Class6 {
 __device__ __forceinline__ Class6 class6(const SegJob& J, uint32_t ci) {
     return Class6{(uint32_t)((J.a + 2 * ci) % 6), (J.delta + 2 * ci) / 6};
 }
-// the three classes of a block, looked up without local memory
+// the three classes of a block, looked up without local memory: r and G of
+// class ci follow from a mod 6 and delta (two registers, not six)
 struct Classes6 {
-    uint32_t r0, r1, r2, G0, G1, G2;
-    __device__ __forceinline__ explicit Classes6(const SegJob& J) {
-        const uint32_t a6 = (uint32_t)(J.a % 6);
-        r0 = a6;
-        r1 = (a6 + 2) % 6;
-        r2 = (a6 + 4) % 6;
-        G0 = J.delta / 6;
-        G1 = (J.delta + 2) / 6;
-        G2 = (J.delta + 4) / 6;
-    }
+    uint32_t a6, delta;
+    __device__ __forceinline__ explicit Classes6(const SegJob& J) : a6((uint32_t)(J.a % 6)), delta(J.delta) {}
     __device__ __forceinline__ Class6 operator[](uint32_t ci) const {
-        return Class6{ci == 0 ? r0 : ci == 1 ? r1 : r2, ci == 0 ? G0 : ci == 1 ? G1 : G2};
+        uint32_t r = a6 + 2 * ci;
+        r = r >= 6 ? r - 6 : r;
+        return Class6{r, (delta + 2 * ci) / 6};
     }
 };
 
