@@ -28,18 +28,20 @@ constexpr int TILE_WORDS = W / 32;      // u32 words of the window
 constexpr int THREADS = W_LOG2 >= 20 ? 1024 : 512; // threads per CTA of the fused kernel
 constexpr int CTAS_PER_SM = W_LOG2 >= 20 ? 1 : 2;
 constexpr int NWARPS = THREADS / 32;
-// Warp-specialised fused kernel (k_verify_ws): one CTA of WS_THREADS per SM,
+// Warp-specialised fused kernel (k_verify_ws): one CTA of WS_THREADS per SM
+// (896: 73 registers per thread, fewer spills than 1024 at equal throughput),
 // 32 SW sieve threads + the rest checking.  Two splits are compiled; the host
 // takes the heavy-sieve one when the block's tile primes exceed
-// WS_HEAVY_PRIMES (measured: 12 sieve warps best at 1e12, 16 at 1e13).
+// WS_HEAVY_PRIMES (measured at 896 threads: 10 sieve warps best at 1e12,
+// 14 at 1e13).
 #ifndef GB_WS_SW_LIGHT
-#define GB_WS_SW_LIGHT 12
+#define GB_WS_SW_LIGHT 10
 #endif
 #ifndef GB_WS_SW_HEAVY
-#define GB_WS_SW_HEAVY 16
+#define GB_WS_SW_HEAVY 14
 #endif
 #ifndef GB_WS_THREADS
-#define GB_WS_THREADS 1024
+#define GB_WS_THREADS 896
 #endif
 constexpr int WS_THREADS = GB_WS_THREADS;
 constexpr int WS_SW_LIGHT = GB_WS_SW_LIGHT, WS_SW_HEAVY = GB_WS_SW_HEAVY;
