@@ -811,9 +811,14 @@ __device__ __forceinline__ uint32_t idx_sum(uint32_t x) {
 // sums of z (VPL planes), FC = per-position found counts (FPL planes);
 // p = 3 + 2z, so the sum is 2 sum_b 2^b idx(V_b) + 3 sum_k 2^k idx(FC_k).
 // Resets V and FC.
-constexpr uint32_t VFLUSH = 4; // words per vertical-counter reduction
-constexpr int VPL = NPL + 2;   // 4 * 127 < 2^9
-constexpr int FPL = 3;         // 4 < 2^3
+#ifndef GB_VFLUSH
+#define GB_VFLUSH 8
+#endif
+constexpr uint32_t VFLUSH = GB_VFLUSH; // words per vertical-counter reduction
+constexpr int ilog2c(uint32_t x) { return x <= 1 ? 0 : 1 + ilog2c((x + 1) / 2); } // ceil(log2 x)
+constexpr int VPL = NPL + ilog2c(VFLUSH);   // VFLUSH * (2^NPL - 1) < 2^VPL
+constexpr int FPL = ilog2c(VFLUSH + 1);     // VFLUSH < 2^FPL
+static_assert(VFLUSH * ((1u << NPL) - 1) < (1u << VPL) && VFLUSH < (1u << FPL), "counter widths");
 __device__ __forceinline__ uint32_t vsum_by_index(uint32_t (&V)[VPL], uint32_t (&FC)[FPL]) {
     uint32_t q = 0;
 #pragma unroll
