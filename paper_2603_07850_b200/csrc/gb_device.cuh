@@ -32,13 +32,13 @@ constexpr int NWARPS = THREADS / 32;
 // (896: 73 registers per thread, fewer spills than 1024 at equal throughput),
 // 32 SW sieve threads + the rest checking.  Two splits are compiled; the host
 // takes the heavy-sieve one when the block's tile primes exceed
-// WS_HEAVY_PRIMES (measured at 896 threads: 10 sieve warps best at 1e12,
-// 14 at 1e13).
+// WS_HEAVY_PRIMES (measured at 896 threads: 12 sieve warps best at 1e12,
+// 15-16 at 1e13).
 #ifndef GB_WS_SW_LIGHT
-#define GB_WS_SW_LIGHT 10
+#define GB_WS_SW_LIGHT 12
 #endif
 #ifndef GB_WS_SW_HEAVY
-#define GB_WS_SW_HEAVY 14
+#define GB_WS_SW_HEAVY 16
 #endif
 #ifndef GB_WS_THREADS
 #define GB_WS_THREADS 896
