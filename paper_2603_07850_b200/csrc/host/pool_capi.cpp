@@ -31,6 +31,7 @@ struct ShmHeader {
     uint64_t magic;
     uint64_t start, limit, span;
     std::atomic<uint64_t> cursor;
+    std::atomic<uint32_t> attached; // processes on this cursor (the tail-limit hint)
 };
 constexpr uint64_t kMagic = 0x474f4c4442414348ull; // "GOLDBACH"
 
@@ -95,6 +96,7 @@ int gb_pool_create(uint64_t start, uint64_t limit, uint64_t seg_size, const char
                 p->shm->limit = limit;
                 p->shm->span = 2 * seg_size;
                 new (&p->shm->cursor) std::atomic<uint64_t>(start);
+                new (&p->shm->attached) std::atomic<uint32_t>(0);
                 std::atomic_thread_fence(std::memory_order_release);
                 p->shm->magic = kMagic;
             } else if (p->shm->magic != kMagic || p->shm->start != start || p->shm->limit != limit ||
@@ -102,7 +104,8 @@ int gb_pool_create(uint64_t start, uint64_t limit, uint64_t seg_size, const char
                 munmap(m, sizeof(ShmHeader));
                 throw ParamError("gb_pool_create: shared pool " + p->name + " does not match these bounds");
             }
-            p->pool = std::make_unique<WorkPool>(start, limit, seg_size, &p->shm->cursor);
+            p->shm->attached.fetch_add(1, std::memory_order_relaxed);
+            p->pool = std::make_unique<WorkPool>(start, limit, seg_size, &p->shm->cursor, &p->shm->attached);
         }
         *out = p.release();
         return GB_OK;
@@ -140,7 +143,7 @@ int gb_drain_pool(gb_dev* dev, gb_pool* pool, int max_inflight, gb_run_result* o
     int depth = 1, inflight = 0;
     bool exhausted = false, stop = false;
     for (;;) {
-        while (!exhausted && !stop && inflight < depth) {
+        while (!exhausted && !stop && inflight < std::min(depth, pool->pool->tail_limit(cap))) {
             auto job = pool->pool->claim_next();
             if (!job) {
                 exhausted = true;
