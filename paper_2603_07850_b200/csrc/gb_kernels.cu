@@ -644,7 +644,10 @@ struct K3Acc {
 // over 64-wide windows of g = p div 6, from the first window with an
 // unscanned candidate.
 constexpr uint32_t PBS = BS6_PMAX;
-constexpr uint32_t DEEP_J0 = ((PBS + 1) / 6) / 64;
+// first deep window per class: the first window with an unscanned candidate
+constexpr uint32_t DEEP_J0_R0 = ((BS6_PMAX_R0 + 1) / 6) / 64;
+constexpr uint32_t DEEP_J0_R24 = ((BS6_PMAX_R24 + 1) / 6) / 64;
+__device__ __forceinline__ uint32_t deep_j0(uint32_t r) { return r == 0 ? DEEP_J0_R0 : DEEP_J0_R24; }
 constexpr int NPL = BS6_PLANES;          // z planes
 constexpr uint32_t QCAP = 512;           // per-warp deep-even queue (classes 2, 4 run ~2x the mean deep rate)
 
@@ -707,7 +710,7 @@ __device__ __forceinline__ void deep_even6(const uint32_t* tile, const uint64_t*
                                            const VerifyArgs& A, uint32_t jlim_small, K3Acc& acc) {
     GB_STAT(1, 1);
     uint32_t p = 0;
-    for (uint32_t j = DEEP_J0; j < (uint32_t)NWIN6 && !p; ++j)
+    for (uint32_t j = deep_j0(C.r); j < (uint32_t)NWIN6 && !p; ++j)
         p = window_hit6(tile, masks6, C.r, C.G, t, j, ~0ull, ~0ull, ~0ull);
     const uint32_t il = ci + 3 * t;
     if (p) acc.add(p, il);
@@ -1037,7 +1040,7 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
                 if (qn + total <= QCAP) {
                     uint32_t pos = qn + pre;
                     const uint32_t t0 = 32 * w - delta; // wraps for w = 0; t0 + bit >= 0 for valid bits
-                    const uint32_t hi = (ci << 18) | (DEEP_J0 << 20);
+                    const uint32_t hi = (ci << 18) | (deep_j0(C.r) << 20);
                     while (U) {
                         const uint32_t bit = __ffs(U) - 1;
                         U &= U - 1;

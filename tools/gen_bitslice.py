@@ -91,7 +91,7 @@ def scan6_words(pmax):
     return gmax // 32 + 2
 
 
-def gen_scan6(name, r, pmax):
+def gen_scan6(name, r, pmax, nplanes=None, nw=None):
     """Wheel-6 scan for the words of evens n = r (mod 6).  The tile holds
     two arrays, A: q = Q + 6k (q = 1 mod 6) and B: q = Q + 4 + 6k (q = 5 mod 6);
     lane bit i of word w is class-r even t = 32w - delta + i, whose candidate
@@ -115,11 +115,12 @@ def gen_scan6(name, r, pmax):
         elif q == 5:
             cands.append((p, "b", (p + 4 - eps) // 6))
     zs = [(p - 3) // 2 for p, _, _ in cands]
-    zmax = (pmax - 3) // 2
-    nplanes = zmax.bit_length()
+    if nplanes is None:
+        nplanes = ((pmax - 3) // 2).bit_length()
     L = []
     L.append(f"// class r = {r}: {len(cands)} candidates p <= {pmax}; planes Z[0..{nplanes - 1}] of z = (p - 3)/2")
-    nw = scan6_words(pmax)  # words per array: WB-(nw-1) .. WB
+    if nw is None:
+        nw = scan6_words(pmax)  # words per array: WB-(nw-1) .. WB
     args = ", ".join([f"uint32_t a{k}" for k in range(nw)] + [f"uint32_t b{k}" for k in range(nw)])
     L.append(f"__device__ __forceinline__ void {name}({args}, uint32_t& U, uint32_t (&Z)[{nplanes}]) {{")
     L.append("    uint32_t S;")
@@ -158,6 +159,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shf-every", type=int, default=1)
     ap.add_argument("--pbs6", type=int, default=385, help="largest bit-sliced candidate (wheel-6 scans)")
+    ap.add_argument("--pbs-r0", type=int, default=257, help="class-0 bound (0: --pbs6)")
+    ap.add_argument("--pbs-r24", type=int, default=449, help="classes 2/4 bound (0: --pbs6)")
     args = ap.parse_args()
     parts = []
     parts.append(f"// gb_bitslice.cuh -- GENERATED by tools/gen_bitslice.py --shf-every {args.shf_every}; do not edit.")
@@ -172,11 +175,18 @@ def main():
     parts.append("namespace gbk {")
     parts.append("")
     parts.append("// ---- wheel-6 layout (k_verify_ws): one scan per residue class of n mod 6")
-    for r in (0, 2, 4):
-        code, n, npl, nw = gen_scan6(f"bs6_scan_r{r}", r, args.pbs6)
+    pr0 = args.pbs_r0 or args.pbs6
+    pr24 = args.pbs_r24 or args.pbs6
+    pmax = max(pr0, pr24)
+    npl = ((pmax - 3) // 2).bit_length()
+    nw = scan6_words(pmax)
+    for r, pm in ((0, pr0), (2, pr24), (4, pr24)):
+        code, n, _, _ = gen_scan6(f"bs6_scan_r{r}", r, pm, nplanes=npl, nw=nw)
         parts.append("")
         parts.append(code)
-    parts.append(f"constexpr uint32_t BS6_PMAX = {args.pbs6};   // candidates p <= BS6_PMAX are bit-sliced")
+    parts.append(f"constexpr uint32_t BS6_PMAX_R0 = {pr0};   // class 0 scans p <= BS6_PMAX_R0")
+    parts.append(f"constexpr uint32_t BS6_PMAX_R24 = {pr24};  // classes 2, 4 scan p <= BS6_PMAX_R24")
+    parts.append(f"constexpr uint32_t BS6_PMAX = {pmax};")
     parts.append(f"constexpr int BS6_PLANES = {npl};")
     parts.append(f"constexpr int BS6_WORDS = {nw};    // tile words per array a scan reads (WB-{nw - 1} .. WB)")
     parts.append("")
