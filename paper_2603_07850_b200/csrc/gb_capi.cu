@@ -101,7 +101,6 @@ struct gb_dev {
     uint64_t* d_m64 = nullptr;          // floor(2^64 / p) per base prime
     uint64_t iL0 = 0, iL1 = 0;          // large primes
     uint32_t* d_pat = nullptr;
-    uint64_t* d_pmr = nullptr;
     uint32_t* d_pat6 = nullptr;         // wheel-6 presieve patterns
     uint64_t* d_masks6 = nullptr;       // wheel-6 deep-window masks
     uint64_t max_piece = 0;
@@ -500,10 +499,9 @@ static int device_odd_primes_upto(gb_dev* d, uint64_t L, uint32_t** d_out, uint6
 
 static int build_tables(gb_dev* d) {
     CU(d, dmalloc(d->device, &d->d_pat, PAT_WORDS * 4));
-    CU(d, dmalloc(d->device, &d->d_pmr, NWIN * 8));
     CU(d, dmalloc(d->device, &d->d_pat6, PAT6_WORDS * 4));
     CU(d, dmalloc(d->device, &d->d_masks6, 3 * NWIN6 * 8));
-    CU(d, launch_init_tables(d->d_pat, d->d_pmr, d->d_pat6, d->d_masks6, d->prm.p_small, d->sync.st));
+    CU(d, launch_init_tables(d->d_pat, d->d_pat6, d->d_masks6, d->prm.p_small, d->sync.st));
     d->launches++;
     int rc = device_odd_primes_upto(d, d->sqrt_bound, &d->d_primes, &d->n_primes);
     if (rc) return rc;
@@ -640,7 +638,6 @@ int gb_close(gb_dev* d) {
     dfree(d->device, d->d_primes);
     dfree(d->device, d->flush_buf);
     dfree(d->device, d->d_pat);
-    dfree(d->device, d->d_pmr);
     dfree(d->device, d->d_pat6);
     dfree(d->device, d->d_masks6);
     dfree(d->device, d->d_wsplit);

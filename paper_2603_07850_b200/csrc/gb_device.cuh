@@ -8,26 +8,16 @@
 namespace gbk {
 
 // ---------------------------------------------------------------- geometry
-// A "block" is the unit one CTA sieves and checks: W odd cells (bits) in
-// shared memory.  Cell w of a block covers the odd q = q_w + 2w.  The top
-// JH cells of the window below the first even's q-top form the Phase 1
-// halo: even n checks candidates p = 3 + 2j, j < JH (p <= 8193), against the
-// cell of n - p.  Evens whose minimal p is not found in-tile are handed to
-// the straggler kernel (K4), which continues the same ascending scan.
-constexpr int JH = 4096;                // in-tile Phase 1 candidates j < JH
-constexpr int NWIN = JH / 64;           // 64-candidate windows
-#ifndef GB_W_LOG2
-#define GB_W_LOG2 19
-#endif
-constexpr int W_LOG2 = GB_W_LOG2;
-constexpr uint32_t W = 1u << W_LOG2;    // cells per block window
-constexpr uint32_t E = W - JH;          // evens per block
+// Odd-only tile of the base-prime sieve (K1, k_sieve_interval): W odd cells
+// (bits), cell w covers q = q_w + 2w.  JH = 4096 fixes the in-tile Phase 1
+// range of the fused kernel: candidates p = 3 + 2j, j < JH (p <= 8193); evens
+// whose minimal p is beyond it go to the straggler kernel (K4), which
+// continues the same ascending scan from j = JH.
+constexpr int JH = 4096;
+constexpr int W_LOG2 = 19;
+constexpr uint32_t W = 1u << W_LOG2;    // cells per K1 window
 constexpr int TILE_WORDS = W / 32;      // u32 words of the window
-// one 1024-thread CTA per SM with a 128 KiB tile (W = 2^20), or two
-// 512-thread CTAs with 64 KiB tiles (W = 2^19): 32 warps per SM either way
-constexpr int THREADS = W_LOG2 >= 20 ? 1024 : 512; // threads per CTA of the fused kernel
-constexpr int CTAS_PER_SM = W_LOG2 >= 20 ? 1 : 2;
-constexpr int NWARPS = THREADS / 32;
+constexpr int THREADS = 512;            // threads per CTA of k_sieve_interval
 // Warp-specialised fused kernel (k_verify_ws): one CTA of WS_THREADS per SM
 // (896: 73 registers per thread, fewer spills than 1024 at equal throughput),
 // 32 SW sieve threads + the rest checking.  Two splits are compiled; the host
@@ -177,16 +167,6 @@ __device__ __forceinline__ uint64_t first_cell_magic(uint64_t q_w, uint64_t p, u
     return d >> 1;
 }
 #endif
-
-// x mod p for p >= 1024, x < 2^32, via an fp32 reciprocal estimate; the
-// estimate is off by at most 2, fixed by the correction loops.
-__device__ __forceinline__ uint32_t mod_fp(uint32_t x, uint32_t p, float rp) {
-    uint32_t q = __float2uint_rz(__uint2float_rz(x) * rp);
-    int32_t r = (int32_t)(x - q * p);
-    while (r < 0) r += (int32_t)p;
-    while (r >= (int32_t)p) r -= (int32_t)p;
-    return (uint32_t)r;
-}
 
 // ------------------------------------------------ Miller-Rabin (K4)
 // Deterministic for n < 2^64 with witnesses {2..37}: the same decision

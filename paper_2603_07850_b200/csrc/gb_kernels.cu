@@ -36,9 +36,8 @@ __device__ unsigned long long g_stats[8];
 #endif
 
 // ============================================================ table init
-// Presieve patterns (odd-only for K1, wheel-6 for the fused kernel), the
-// reversed Phase 1 prime masks of K1's parity hook, and the wheel-6 deep
-// masks: masks6[c * NWIN6 + j] bit 63 - m set iff p = 6 g + off_c (g = 64 j
+// Presieve patterns (odd-only for K1, wheel-6 for the fused kernel) and the
+// wheel-6 deep masks: masks6[c * NWIN6 + j] bit 63 - m set iff p = 6 g + off_c (g = 64 j
 // + m; off = +1, -1, +5 for c = 0, 1, 2) is prime, 5 <= p <= min(p_small, PH6).
 __device__ bool small_prime(uint32_t p) {
     if (p < 2) return false;
@@ -47,7 +46,7 @@ __device__ bool small_prime(uint32_t p) {
     return true;
 }
 
-__global__ void k_init_tables(uint32_t* pat, uint64_t* pmr, uint32_t* pat6, uint64_t* masks6, uint64_t p_small) {
+__global__ void k_init_tables(uint32_t* pat, uint32_t* pat6, uint64_t* masks6, uint64_t p_small) {
     const uint32_t gp[4][3] = {{3, 5, 7}, {17, 19, 23}, {29, 31, 37}, {41, 43, 47}};
     const uint32_t gp1x[2] = {11, 13};
     uint32_t tid = blockIdx.x * blockDim.x + threadIdx.x;
@@ -81,17 +80,6 @@ __global__ void k_init_tables(uint32_t* pat, uint64_t* pmr, uint32_t* pat6, uint
             }
             pat6[pg6_off(g) + w] = v;
         }
-    }
-    // pmr[k] bit (63 - j') set iff p = 3 + 2(64k + j') is prime and <= p_small
-    for (uint32_t k = tid; k < (uint32_t)NWIN; k += nthr) {
-        uint64_t m = 0;
-        for (int jp = 0; jp < 64; ++jp) {
-            uint32_t p = 3 + 2 * (64 * k + jp);
-            bool pr = p <= p_small;
-            for (uint32_t d = 3; pr && d * d <= p; d += 2) pr = (p % d) != 0;
-            if (pr) m |= 1ull << (63 - jp);
-        }
-        pmr[k] = m;
     }
     const uint64_t pmax = p_small < PH6 ? p_small : PH6;
     for (uint32_t e = tid; e < 3u * NWIN6; e += nthr) {
@@ -129,9 +117,6 @@ __global__ void k_seed_primes(uint32_t lim, uint32_t* out, uint32_t* count) {
 // Presieve (patterns), fix-ups and strikes of one W-cell window in shared
 // memory.  OffsetFn(i, p) returns the window cell of the first odd multiple
 // of p >= max(p^2, q_w), or >= W when p does not strike the window.
-struct SmemTables {
-    uint32_t pat[PAT_WORDS];
-};
 
 __device__ __forceinline__ void presieve_window(uint32_t* tile, const uint32_t* pat, uint64_t q_w, uint32_t tid,
                                                 uint32_t nthr) {
@@ -1403,9 +1388,8 @@ cudaError_t launch_smem_peak(uint32_t iters, uint32_t* sink, int grid, cudaStrea
     k_smem_peak<<<grid, SMEM_PEAK_THREADS, 65536, st>>>(iters, sink);
     return cudaGetLastError();
 }
-cudaError_t launch_init_tables(uint32_t* pat, uint64_t* pmr, uint32_t* pat6, uint64_t* masks6, uint64_t p_small,
-                               cudaStream_t st) {
-    k_init_tables<<<64, 256, 0, st>>>(pat, pmr, pat6, masks6, p_small);
+cudaError_t launch_init_tables(uint32_t* pat, uint32_t* pat6, uint64_t* masks6, uint64_t p_small, cudaStream_t st) {
+    k_init_tables<<<64, 256, 0, st>>>(pat, pat6, masks6, p_small);
     return cudaGetLastError();
 }
 cudaError_t launch_seed_primes(uint32_t lim, uint32_t* out, uint32_t* count, cudaStream_t st) {

@@ -56,8 +56,7 @@ constexpr uint32_t WS_MASK_OFF = (WS_PAT_OFF + PAT6_WORDS + 3) & ~3u;
 constexpr size_t WS_SMEM = (size_t)WS_MASK_OFF * 4 + 3 * NWIN6 * 8;
 
 // ---- launchers (gb_kernels.cu); all asynchronous on `st`
-cudaError_t launch_init_tables(uint32_t* pat, uint64_t* pmr, uint32_t* pat6, uint64_t* masks6, uint64_t p_small,
-                               cudaStream_t st);
+cudaError_t launch_init_tables(uint32_t* pat, uint32_t* pat6, uint64_t* masks6, uint64_t p_small, cudaStream_t st);
 cudaError_t launch_seed_primes(uint32_t lim, uint32_t* out, uint32_t* count, cudaStream_t st);
 cudaError_t launch_sieve_interval(uint64_t lo, uint64_t n_cells, const uint32_t* primes, uint32_t iA0,
                                   uint32_t iA1, uint32_t iB1, const uint32_t* pat, uint32_t* out,
