@@ -91,7 +91,7 @@ def scan6_words(pmax):
     return gmax // 32 + 2
 
 
-def gen_scan6(name, r, pmax, nplanes=None, nw=None):
+def gen_scan6(name, r, pmax, nplanes=None, nw=None, fma_every=0):
     """Wheel-6 scan for the words of evens n = r (mod 6).  The tile holds
     two arrays, A: q = Q + 6k (q = 1 mod 6) and B: q = Q + 4 + 6k (q = 5 mod 6);
     lane bit i of word w is class-r even t = 32w - delta + i, whose candidate
@@ -140,7 +140,12 @@ def gen_scan6(name, r, pmax, nplanes=None, nw=None):
         sh = (-g) % 32
         w = [f"{arr}{i}" for i in range(nw)]  # w[nw-1] = word WB
         top = nw - 1
-        src = w[top - k] if sh == 0 else f"__funnelshift_r({w[top - k]}, {w[top - k + 1]}, {sh})"
+        if sh == 0:
+            src = w[top - k]
+        elif fma_every and idx % fma_every == 0:
+            src = f"fsr_fma({w[top - k]}, {w[top - k + 1]}, {sh})"
+        else:
+            src = f"__funnelshift_r({w[top - k]}, {w[top - k + 1]}, {sh})"
         L.append(f"    S = {src}; // p = {p}")
         L.append("    U &= ~S;")
         for b in range(nplanes):
@@ -160,6 +165,8 @@ def main():
     ap.add_argument("--shf-every", type=int, default=1)
     ap.add_argument("--pbs6", type=int, default=385, help="largest bit-sliced candidate (wheel-6 scans)")
     ap.add_argument("--pbs-r0", type=int, default=257, help="class-0 bound (0: --pbs6)")
+    ap.add_argument("--fma-every", type=int, default=0,
+                    help="every N-th candidate's funnel shift on the FMA pipe (0: none)")
     ap.add_argument("--pbs-r24", type=int, default=449, help="classes 2/4 bound (0: --pbs6)")
     args = ap.parse_args()
     parts = []
@@ -174,6 +181,15 @@ def main():
     parts.append("")
     parts.append("namespace gbk {")
     parts.append("")
+    if args.fma_every:
+        parts.append("// 2^k; in constant memory so the IMAD funnel below is not folded into SHF")
+        parts.append("__constant__ uint32_t c_pow2[32] = {" + ", ".join(f"{1 << k}u" for k in range(32)) + "};")
+        parts.append("// funnel shift right of (hi:lo) by sh (0 < sh < 32) on the FMA pipe")
+        parts.append("__device__ __forceinline__ uint32_t fsr_fma(uint32_t lo, uint32_t hi, int sh) {")
+        parts.append("    const uint32_t K = c_pow2[32 - sh];")
+        parts.append("    return hi * K + __umulhi(lo, K);")
+        parts.append("}")
+        parts.append("")
     parts.append("// ---- wheel-6 layout (k_verify_ws): one scan per residue class of n mod 6")
     pr0 = args.pbs_r0 or args.pbs6
     pr24 = args.pbs_r24 or args.pbs6
@@ -181,7 +197,7 @@ def main():
     npl = ((pmax - 3) // 2).bit_length()
     nw = scan6_words(pmax)
     for r, pm in ((0, pr0), (2, pr24), (4, pr24)):
-        code, n, _, _ = gen_scan6(f"bs6_scan_r{r}", r, pm, nplanes=npl, nw=nw)
+        code, n, _, _ = gen_scan6(f"bs6_scan_r{r}", r, pm, nplanes=npl, nw=nw, fma_every=args.fma_every)
         parts.append("")
         parts.append(code)
     parts.append(f"constexpr uint32_t BS6_PMAX_R0 = {pr0};   // class 0 scans p <= BS6_PMAX_R0")
