@@ -175,6 +175,13 @@ int gb_launch_count(const gb_dev* dev, uint64_t* launches);
  * (K2/K3 fused), [1]=large-prime strike, [2]=stragglers/Phase 2, [3]=other. */
 int gb_kernel_times(gb_dev* dev, double* ms4, uint64_t* launches4, int reset);
 
+/* Debug counters of the fused kernel, process-wide (builds with
+ * -DGB_STATS only; GB_ERR_PARAM otherwise): [0] evens checked per even on
+ * the generic path, [1] deep evens resolved in place (queue overflow),
+ * [2] deep evens queued, [3] deep rounds, [4] straggler entries, [5] fast
+ * blocks, [6] generic blocks.  Not part of the reference interface. */
+int gb_debug_stats(uint64_t* out8, int reset);
+
 /* Per-launch event timing: 0 off, 1 on, 2 on with every batch serialised on
  * one stream (so an event pair brackets exactly one kernel's execution;
  * used for the roofline pass of bench.py).  No segments may be pending. */
