@@ -71,3 +71,24 @@ def test_p_small_around_the_fast_path(gpu, p_small):
     a, b = 10**9, 10**9 + 2 * 100_000
     with gpu.Device(b, p_small=p_small) as dev:
         same(dev.verify_segment(a, b), oracle.verify_segment(a, b, cover=b, p_small=p_small))
+
+
+def test_reference_known_answers(gpu):
+    # [4, 1e4]: 4,999 evens, max 173 @ 7426 (test_verifier.cpp:265-282);
+    # p_min on [4, 20] = {2,3,3,3,5,3,3,5,3}, max 5 @ 12 (:59-73);
+    # pi(1e9) = 50,847,534 (test_sieve.cpp:188-200)
+    with gpu.Device(10**4) as dev:
+        r = dev.verify_segment(4, 10**4).as_dict()
+        assert (r["evens"], r["max_p"], r["max_n"], r["unverified"]) == (4_999, 173, 7426, 0)
+        assert [int(x) for x in dev.phase1_pmin(4, 20)] == [2, 3, 3, 3, 5, 3, 3, 5, 3]
+    with gpu.Device(10**9) as dev:
+        assert len(dev.primes_upto(10**9)) == 50_847_534 - 1  # odd primes (2 excluded)
+
+
+def test_pmin_window_above_1e12(gpu):
+    # per-n p_min on [1e12, 1e12 + 400] (test_verifier.cpp:330-349) vs the oracle
+    a, b = 10**12, 10**12 + 400
+    with gpu.Device(b) as dev:
+        got = dev.phase1_pmin(a, b)
+    want = np.array(oracle.phase1_pmin(a, b, cover=b), dtype=np.uint64)
+    assert (got == want).all()
