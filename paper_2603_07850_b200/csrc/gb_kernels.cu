@@ -836,6 +836,92 @@ __device__ __forceinline__ void scan_word6(const uint32_t* tile, uint32_t r, uin
     else bs6_scan_r4(a0, a1, a2, a3, b0, b1, b2, b3, U, Z);
 }
 
+// Sums of one scanned word: sum p (weighted by the word's even index), and
+// its z planes / found bits into the vertical counters.
+template <bool PMIN>
+__device__ __forceinline__ void word_sums(const VerifyArgs& A, uint32_t w, uint32_t valid, uint32_t U,
+                                          const uint32_t (&Z)[NPL], uint32_t ci, uint32_t delta, uint32_t i0,
+                                          uint32_t (&V)[VPL], uint32_t (&FC)[FPL], uint32_t& sp32, K3Acc& acc) {
+    const uint32_t F = valid & ~U;
+    // p = 3 + 2z: sum p of the word; il = ci + 3 (32w - delta + i)
+    uint32_t P = 3 * __popc(F);
+#pragma unroll
+    for (int bp = 0; bp < NPL; ++bp) P += (2u << bp) * __popc(Z[bp]);
+    sp32 += P;
+    acc.spi += (uint64_t)P * (uint64_t)((int64_t)ci + 96 * (int64_t)w - 3 * (int64_t)delta);
+    // V += Z, FC += F (ripple-carry, bit-sliced)
+    uint32_t cy = V[0] & Z[0];
+    V[0] ^= Z[0];
+#pragma unroll
+    for (int bp = 1; bp < NPL; ++bp) {
+        const uint32_t v = V[bp], z = Z[bp];
+        V[bp] = v ^ z ^ cy;
+        cy = (v & z) | (cy & (v ^ z));
+    }
+#pragma unroll
+    for (int bp = NPL; bp < VPL; ++bp) {
+        const uint32_t v = V[bp];
+        V[bp] = v ^ cy;
+        cy = v & cy;
+    }
+    cy = F;
+#pragma unroll
+    for (int kk = 0; kk < FPL; ++kk) {
+        const uint32_t f = FC[kk];
+        FC[kk] = f ^ cy;
+        cy = f & cy;
+    }
+    if constexpr (PMIN) {
+        for (uint32_t i = 0; i < 32; ++i) {
+            if (!((F >> i) & 1)) continue;
+            uint32_t z = 0;
+#pragma unroll
+            for (int bp = 0; bp < NPL; ++bp) z |= ((Z[bp] >> i) & 1) << bp;
+            A.pmin_out[i0 + ci + 3 * (32 * w - delta + i)] = 3 + 2 * z;
+        }
+    }
+}
+
+// Deep evens of one word (U): appended to the warp's round queue, positions
+// from a ballot per count threshold (counts are 0..2 almost always); full
+// rounds run as soon as 32 entries wait.  Warp-uniform call.
+template <bool PMIN>
+__device__ __forceinline__ uint32_t word_deep(const uint32_t* tile, const uint64_t* masks6, uint32_t* q, uint32_t qn,
+                                              uint32_t U, uint32_t w, uint32_t ci, uint32_t delta, const Class6 C,
+                                              uint32_t lane, uint32_t i0, uint32_t s, const SegJob& J,
+                                              const Classes6& CL, const VerifyArgs& A, uint32_t jlim_small,
+                                              K3Acc& acc) {
+    const uint32_t cnt = __popc(U);
+    const uint32_t cmax = __reduce_max_sync(0xffffffffu, cnt);
+    if (cmax == 0) return qn;
+    const uint32_t total = __reduce_add_sync(0xffffffffu, cnt);
+    const uint32_t lt = (1u << lane) - 1;
+    uint32_t pre = 0;
+    for (uint32_t th = 1; th <= cmax; ++th) pre += __popc(__ballot_sync(0xffffffffu, cnt >= th) & lt);
+    if (lane == 0) GB_STAT(2, total);
+    if (qn + total <= QCAP) {
+        uint32_t pos = qn + pre;
+        const uint32_t t0 = 32 * w - delta; // wraps for w = 0; t0 + bit >= 0 for valid bits
+        const uint32_t hi = (ci << 18) | (deep_j0(C.r) << 20);
+        while (U) {
+            const uint32_t bit = __ffs(U) - 1;
+            U &= U - 1;
+            q[pos++] = (t0 + bit) | hi;
+        }
+        qn += total;
+        __syncwarp();
+        while (qn >= 32) qn = deep_round6<PMIN>(tile, masks6, q, qn, 32, lane, i0, s, J, CL, A, jlim_small, acc);
+    } else {
+        while (U) { // queue full: this lane's deep evens in place
+            const uint32_t bit = __ffs(U) - 1;
+            U &= U - 1;
+            deep_even6<PMIN>(tile, masks6, 32 * w - delta + bit, C, ci, i0, s, J, A, jlim_small, acc);
+        }
+        __syncwarp();
+    }
+    return qn;
+}
+
 // Valid bits of word w of a class with T evens and alignment delta.
 __device__ __forceinline__ uint32_t word_mask6(uint32_t w, uint32_t T, uint32_t delta) {
     uint32_t m = ~0u;
@@ -969,80 +1055,13 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
                     uint32_t Z[NPL];
                     U = valid;
                     scan_word6(tile, C.r, w + (C.G >> 5), U, Z);
-                    const uint32_t F = valid & ~U;
-                    // p = 3 + 2z: sum p of the word; il = ci + 3 (32w - delta + i)
-                    uint32_t P = 3 * __popc(F);
-#pragma unroll
-                    for (int bp = 0; bp < NPL; ++bp) P += (2u << bp) * __popc(Z[bp]);
-                    sp32 += P;
-                    acc.spi += (uint64_t)P * (uint64_t)((int64_t)ci + 96 * (int64_t)w - 3 * (int64_t)delta);
-                    // V += Z, FC += F (ripple-carry, bit-sliced)
-                    uint32_t cy = V[0] & Z[0];
-                    V[0] ^= Z[0];
-#pragma unroll
-                    for (int bp = 1; bp < NPL; ++bp) {
-                        const uint32_t v = V[bp], z = Z[bp];
-                        V[bp] = v ^ z ^ cy;
-                        cy = (v & z) | (cy & (v ^ z));
-                    }
-#pragma unroll
-                    for (int bp = NPL; bp < VPL; ++bp) {
-                        const uint32_t v = V[bp];
-                        V[bp] = v ^ cy;
-                        cy = v & cy;
-                    }
-                    cy = F;
-#pragma unroll
-                    for (int kk = 0; kk < FPL; ++kk) {
-                        const uint32_t f = FC[kk];
-                        FC[kk] = f ^ cy;
-                        cy = f & cy;
-                    }
-                    if constexpr (PMIN) {
-                        for (uint32_t i = 0; i < 32; ++i) {
-                            if (!((F >> i) & 1)) continue;
-                            uint32_t z = 0;
-#pragma unroll
-                            for (int bp = 0; bp < NPL; ++bp) z |= ((Z[bp] >> i) & 1) << bp;
-                            A.pmin_out[i0 + ci + 3 * (32 * w - delta + i)] = 3 + 2 * z;
-                        }
-                    }
+                    word_sums<PMIN>(A, w, valid, U, Z, ci, delta, i0, V, FC, sp32, acc);
                 }
                 if (++nbatch == VFLUSH) { // counters hold VFLUSH words
                     acc.spi += 3ull * vsum_by_index(V, FC);
                     nbatch = 0;
                 }
-                // deep evens of the word: exclusive prefix of the lanes' counts
-                // by ballot per count threshold (counts are 0..2 almost always)
-                const uint32_t cnt = __popc(U);
-                const uint32_t cmax = __reduce_max_sync(0xffffffffu, cnt);
-                if (cmax == 0) continue;
-                const uint32_t total = __reduce_add_sync(0xffffffffu, cnt);
-                const uint32_t lt = (1u << lane) - 1;
-                uint32_t pre = 0;
-                for (uint32_t th = 1; th <= cmax; ++th) pre += __popc(__ballot_sync(0xffffffffu, cnt >= th) & lt);
-                if (lane == 0) GB_STAT(2, total);
-                if (qn + total <= QCAP) {
-                    uint32_t pos = qn + pre;
-                    const uint32_t t0 = 32 * w - delta; // wraps for w = 0; t0 + bit >= 0 for valid bits
-                    const uint32_t hi = (ci << 18) | (deep_j0(C.r) << 20);
-                    while (U) {
-                        const uint32_t bit = __ffs(U) - 1;
-                        U &= U - 1;
-                        q[pos++] = (t0 + bit) | hi;
-                    }
-                    qn += total;
-                    __syncwarp();
-                    while (qn >= 32)
-                        qn = deep_round6<PMIN>(tile, masks6, q, qn, 32, lane, i0, s, J, CL, A, jlim_small, acc);
-                } else {
-                    while (U) { // queue full: this lane's deep evens in place
-                        const uint32_t bit = __ffs(U) - 1;
-                        U &= U - 1;
-                        deep_even6<PMIN>(tile, masks6, 32 * w - delta + bit, CL[ci], ci, i0, s, J, A, jlim_small, acc);
-                    }
-                    __syncwarp();
-                }
+                qn = word_deep<PMIN>(tile, masks6, q, qn, U, w, ci, delta, C, lane, i0, s, J, CL, A, jlim_small, acc);
             }
         }
         while (qn) qn = deep_round6<PMIN>(tile, masks6, q, qn, min(qn, 32u), lane, i0, s, J, CL, A, jlim_small, acc);
