@@ -370,27 +370,63 @@ __global__ void k_segment_offsets(const SegJob* __restrict__ jobs, uint32_t nslo
     }
 }
 
-// Primes above P_TILE_MAX: strike the slot's global wheel-6 bitmask (array A
+// Primes above P_TILE_MAX: strike each slot's global wheel-6 bitmask (array A
 // then array B, qg_words words each, cells relative to the slot's origin)
-// with RED.AND; the fused kernel ANDs the words into its tiles.  Grid: x over
-// primes, y = slot.
-__global__ void k_large_strike(const SegJob* __restrict__ jobs, uint32_t nslots,
-                               const uint32_t* __restrict__ primes, const uint64_t* __restrict__ m64,
-                               uint64_t iL0, uint64_t iL1, uint32_t* __restrict__ qg, uint64_t qg_stride_words) {
-    const uint32_t s = blockIdx.y;
-    const SegJob& j = jobs[s];
-    const uint32_t ncells = j.qg_words * 32;
-    uint32_t* ga = qg + s * qg_stride_words;
-    uint32_t* gb = ga + j.qg_words;
+// with RED.AND; the fused kernel ANDs the words into its tiles.  One thread
+// per prime for every slot of the batch: p and its magic are loaded once, the
+// full first-multiple computation runs for slot 0 only, and a slot whose
+// origin lies d < 2^32 wheel steps above slot 0's (consecutive pool claims)
+// gets its first index as k0 - d mod p with 32-bit arithmetic.
+constexpr uint32_t LS_MAX_SLOTS = 16;
+#ifndef GB_LS_GROUP
+#define GB_LS_GROUP 2
+#endif
+// slots per grid row: the rows run in order, so the REDs of one row hit
+// LS_GROUP slot bitmasks (16.7 MB each at 2e8-even segments) that stay in L2
+constexpr uint32_t LS_GROUP = GB_LS_GROUP;
+
+__global__ void __launch_bounds__(256) k_large_strike(const SegJob* __restrict__ jobs, uint32_t nslots,
+                                                      const uint32_t* __restrict__ primes,
+                                                      const uint64_t* __restrict__ m64, uint64_t iL0, uint64_t iL1,
+                                                      uint32_t* __restrict__ qg, uint64_t qg_stride_words) {
+    __shared__ SegJob s_jobs[LS_MAX_SLOTS];
+    __shared__ uint32_t s_d[LS_MAX_SLOTS], s_near[LS_MAX_SLOTS];
+    if (threadIdx.x < nslots) {
+        const SegJob j = jobs[threadIdx.x], j0 = jobs[0];
+        s_jobs[threadIdx.x] = j;
+        // slot origin Q_s = Q_0 + 6 d with 0 <= d < 2^32 (both positive)
+        const bool near = !j.qneg && !j0.qneg && j.qbase >= j0.qbase && (j.qbase - j0.qbase) / 6 < (1ull << 32);
+        s_near[threadIdx.x] = near;
+        s_d[threadIdx.x] = near ? (uint32_t)((j.qbase - j0.qbase) / 6) : 0;
+    }
+    __syncthreads();
     for (uint64_t i = iL0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < iL1;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t p = primes[i];
-        const uint32_t k0 = first_a6(j, p, m64[i]);
+        const uint64_t m = m64[i];
+        const uint32_t m32 = (uint32_t)(m >> 32); // <= floor(2^32 / p)
+        const uint32_t k00 = first_a6(s_jobs[0], p, m);
         const uint32_t c = b_shift6(p);
-        const uint32_t k0b = k0 >= c ? k0 - c : k0 + p - c;
-        // k + p can pass 2^32 (p < 2^32 near the 2^64 ceiling): 64-bit steps
-        for (uint64_t k = k0; k < ncells; k += p) atomicAnd(&ga[k >> 5], ~(1u << (k & 31)));
-        for (uint64_t k = k0b; k < ncells; k += p) atomicAnd(&gb[k >> 5], ~(1u << (k & 31)));
+        const uint32_t s1 = min(nslots, (blockIdx.y + 1) * LS_GROUP);
+        for (uint32_t s = blockIdx.y * LS_GROUP; s < s1; ++s) {
+            const SegJob& j = s_jobs[s];
+            uint32_t k0;
+            if (s_near[s]) {
+                const uint32_t d = s_d[s];
+                uint32_t r = d - __umulhi(d, m32) * p; // d mod p, quotient low by <= 2
+                while (r >= p) r -= p;
+                k0 = k00 >= r ? k00 - r : k00 + (p - r);
+            } else {
+                k0 = first_a6(j, p, m);
+            }
+            const uint32_t k0b = k0 >= c ? k0 - c : k0 + (p - c);
+            const uint32_t ncells = j.qg_words * 32;
+            uint32_t* ga = qg + s * qg_stride_words;
+            uint32_t* gb = ga + j.qg_words;
+            // k + p can pass 2^32 (p < 2^32 near the 2^64 ceiling): 64-bit steps
+            for (uint64_t k = k0; k < ncells; k += p) atomicAnd(&ga[k >> 5], ~(1u << (k & 31)));
+            for (uint64_t k = k0b; k < ncells; k += p) atomicAnd(&gb[k >> 5], ~(1u << (k & 31)));
+        }
     }
 }
 
@@ -1453,8 +1489,10 @@ cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint3
                                 uint64_t iL0, uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, cudaStream_t st) {
     const uint64_t np = iL1 - iL0;
     if (!np || !nslots) return cudaSuccess;
-    const unsigned gx = (unsigned)std::min<uint64_t>((np + 255) / 256, 148ull * 32 / nslots + 1);
-    k_large_strike<<<dim3(gx, nslots), 256, 0, st>>>(jobs, nslots, primes, m64, iL0, iL1, qg, qg_stride_words);
+    if (nslots > LS_MAX_SLOTS) return cudaErrorInvalidValue;
+    const unsigned gx = (unsigned)std::min<uint64_t>((np + 255) / 256, 148ull * 16);
+    k_large_strike<<<dim3(gx, (nslots + LS_GROUP - 1) / LS_GROUP), 256, 0, st>>>(jobs, nslots, primes, m64, iL0,
+                                                                                 iL1, qg, qg_stride_words);
     return cudaGetLastError();
 }
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st) {

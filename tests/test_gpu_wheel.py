@@ -92,3 +92,24 @@ def test_pmin_window_above_1e12(gpu):
         got = dev.phase1_pmin(a, b)
     want = np.array(oracle.phase1_pmin(a, b, cover=b), dtype=np.uint64)
     assert (got == want).all()
+
+
+def test_large_prime_batches_out_of_order(gpu):
+    # base primes past 2^22, so k_large_strike runs; one batch holds pieces
+    # above, below and far from its first slot (the incremental first-multiple
+    # path applies only to slots 0 <= d < 2^32 wheel steps above slot 0), plus
+    # neighbours 2 * E6 apart (the incremental path)
+    cover = 4 * 10**16
+    base = 10**16
+    n_ev = E6 // 2 + 7
+    starts = [base + 2 * E6 * 4, base, base + 2 * E6 * 8, 3 * 10**16 + 2, base + 2 * E6 * 9,
+              base + 6 * 10**15 + 4, base + 2 * E6 * 4 + 6, 2 * 10**13 + 2]
+    with gpu.Device(cover) as dev:
+        for a in starts:
+            dev.submit(a, a + 2 * (n_ev - 1), tag=a)
+        got = {}
+        for _ in starts:
+            rec, tag = dev.wait()
+            got[tag] = rec
+    for a in starts:
+        same(got[a], oracle.verify_segment(a, a + 2 * (n_ev - 1), cover=cover))
