@@ -423,9 +423,18 @@ __global__ void __launch_bounds__(256) k_large_strike(const SegJob* __restrict__
             const uint32_t ncells = j.qg_words * 32;
             uint32_t* ga = qg + s * qg_stride_words;
             uint32_t* gb = ga + j.qg_words;
-            // k + p can pass 2^32 (p < 2^32 near the 2^64 ceiling): 64-bit steps
-            for (uint64_t k = k0; k < ncells; k += p) atomicAnd(&ga[k >> 5], ~(1u << (k & 31)));
-            for (uint64_t k = k0b; k < ncells; k += p) atomicAnd(&gb[k >> 5], ~(1u << (k & 31)));
+            // 32-bit steps: k < ncells < 2^32 and the step test cannot wrap
+            // (p < 2^32 near the 2^64 ceiling)
+            for (uint32_t k = k0; k < ncells;) {
+                atomicAnd(ga + (k >> 5), ~(1u << (k & 31)));
+                if (p >= ncells - k) break;
+                k += p;
+            }
+            for (uint32_t k = k0b; k < ncells;) {
+                atomicAnd(gb + (k >> 5), ~(1u << (k & 31)));
+                if (p >= ncells - k) break;
+                k += p;
+            }
         }
     }
 }
