@@ -39,7 +39,10 @@ constexpr uint32_t WS_HEAVY_PRIMES = 150000;
 // warps of the group that runs the warp-cooperative strikes (max of the splits)
 constexpr int SPLIT_WARPS = WS_SW_HEAVY > WS_SW_LIGHT ? WS_SW_HEAVY : WS_SW_LIGHT;
 constexpr uint32_t P_TILE_MAX = 1u << 22; // base primes above: K_large (global strikes)
-constexpr uint32_t P_WARP_MAX = 1024;     // primes below: warp-cooperative strikes
+#ifndef GB_P_WARP_MAX
+#define GB_P_WARP_MAX 2048
+#endif
+constexpr uint32_t P_WARP_MAX = GB_P_WARP_MAX; // primes below: warp-cooperative strikes
 constexpr uint32_t FIRST_STRIKE_P = 53;   // primes below are in the presieve patterns
 constexpr uint32_t MAX_SEG_EVENS = 1u << 30; // device sub-segment (piece) limit
 
