@@ -72,7 +72,7 @@ __global__ void k_init_tables(uint32_t* pat, uint32_t* pat6, uint64_t* masks6, u
         for (uint32_t w = tid; w < nw6; w += nthr) {
             uint32_t v = 0;
             for (int bit = 0; bit < 32; ++bit) {
-                const uint64_t val = 6ull * ((w * 32 + bit) % P6) + 1;
+                const uint32_t val = 6u * ((w * 32 + bit) % P6) + 1; // < 6 * 82861 + 1
                 bool comp = false;
                 if (g == 0) comp = val % 5 == 0 || val % 7 == 0 || val % 11 == 0 || val % 13 == 0;
                 else for (int t = 0; t < 3; ++t) comp |= (val % gp[g][t]) == 0;
@@ -81,16 +81,19 @@ __global__ void k_init_tables(uint32_t* pat, uint32_t* pat6, uint64_t* masks6, u
             pat6[pg6_off(g) + w] = v;
         }
     }
+    // one warp per mask word, one candidate per lane and half
     const uint64_t pmax = p_small < PH6 ? p_small : PH6;
-    for (uint32_t e = tid; e < 3u * NWIN6; e += nthr) {
+    const uint32_t lane = threadIdx.x & 31;
+    for (uint32_t e = tid >> 5; e < 3u * NWIN6; e += nthr >> 5) {
         const uint32_t cls = e / NWIN6, j = e % NWIN6;
         const int off = cls == 0 ? 1 : cls == 1 ? -1 : 5;
-        uint64_t m = 0;
-        for (int jm = 0; jm < 64; ++jm) {
-            const int64_t p = 6 * (int64_t)(64 * j + jm) + off;
-            if (p >= 5 && (uint64_t)p <= pmax && small_prime((uint32_t)p)) m |= 1ull << (63 - jm);
+        uint32_t half[2];
+        for (int h = 0; h < 2; ++h) {
+            const int64_t p = 6 * (int64_t)(64 * j + 32 * h + lane) + off;
+            half[h] = __ballot_sync(0xffffffffu, p >= 5 && (uint64_t)p <= pmax && small_prime((uint32_t)p));
         }
-        masks6[e] = m;
+        // bit 63 - jm <-> candidate jm
+        if (lane == 0) masks6[e] = ((uint64_t)__brev(half[0]) << 32) | __brev(half[1]);
     }
 }
 
