@@ -1193,7 +1193,7 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
     if (tid == 0 && K) atomicMax(&A.acc[s].key, (unsigned long long)K);
 }
 
-// Warp-specialised fused kernel: one 1024-thread CTA per SM, two wheel-6
+// Warp-specialised fused kernel: one 896-thread CTA per SM, two wheel-6
 // tile buffers.  The first 32 SW threads (the sieve group) sieve block k
 // into buffer k & 1 while the other threads (the check group) check
 // block k - 1 in the other buffer.  Named barriers hand buffers over:
