@@ -96,3 +96,48 @@ def test_device_phase2_matches_reference(gpu):
             pass
         with gpu.Device(1000, p_small=3) as dev:
             assert dev.phase2_resolve(c["n"]) == c["p"], c
+
+
+def _seg_matches(rec, r):
+    got = rec.as_dict()
+    for k in ("a", "b", "evens", "sum_pmin", "pos_hash", "max_p", "max_n"):
+        assert got[k] == r[k], (k, got, r)
+    assert got["unverified"] == 0 and got["n_ce"] == 0
+
+
+def test_c3_full_range_and_anchors(gpu):
+    # all of C3 through the pool (run_workers) + every 250th segment alone,
+    # against the reference's Appendix A records
+    g = golden("appendix_a_large.json")["c3"]
+    res, _ = gpu.run_range(4, g["limit"])
+    d = res.as_dict()
+    for k in ("evens", "unverified", "sum_pmin", "pos_hash", "max_p", "max_n", "segments"):
+        assert d[k] == g[k], (k, d, g)
+    with gpu.Device(g["limit"]) as dev:
+        for r in g["anchors"]:
+            dev.submit(r["a"], r["b"], tag=r["a"])
+        got = {}
+        for _ in g["anchors"]:
+            rec, tag = dev.wait()
+            got[tag] = rec
+    for r in g["anchors"]:
+        _seg_matches(got[r["a"]], r)
+
+
+def test_c5_window_first_segments(gpu):
+    # base primes to 2e9 (98 M): the large-prime bitmask path, one batch of
+    # 8 consecutive segments (incremental first multiples across slots)
+    g = golden("appendix_a_large.json")["c5_first8"]
+    with gpu.Device(g["cover"]) as dev:
+        for r in g["records"]:
+            dev.submit(r["a"], r["b"], tag=r["a"])
+        got = {}
+        for _ in g["records"]:
+            rec, tag = dev.wait()
+            got[tag] = rec
+    tot_sum = tot_hash = 0
+    for r in g["records"]:
+        _seg_matches(got[r["a"]], r)
+        tot_sum += got[r["a"]].as_dict()["sum_pmin"]
+        tot_hash = (tot_hash + got[r["a"]].as_dict()["pos_hash"]) % (1 << 64)
+    assert (tot_sum, tot_hash) == (g["sum_pmin"], g["pos_hash"])
