@@ -853,9 +853,30 @@ __device__ __forceinline__ uint32_t idx_sum(uint32_t x) {
 constexpr uint32_t VFLUSH = GB_VFLUSH; // words per vertical-counter reduction
 constexpr int ilog2c(uint32_t x) { return x <= 1 ? 0 : 1 + ilog2c((x + 1) / 2); } // ceil(log2 x)
 constexpr int VPL = NPL + ilog2c(VFLUSH);   // VFLUSH * (2^NPL - 1) < 2^VPL
+#if BS6_CODE
+// class code c: p = 3c + kf F + ke Z0 (gen_bitslice.py class_code), and
+// kf F + ke Z0 = sg (g0 + 2 g1) with g0 = F & ~Z0, g1 = Z0 (class 0) or 0,
+// sg = -1 for class 4, else +1.  FC counts g0 + 2 g1 per position.
+constexpr int FPL = ilog2c(2 * VFLUSH + 1); // 2 VFLUSH < 2^FPL
+static_assert(VFLUSH * ((1u << NPL) - 1) < (1u << VPL) && 2 * VFLUSH < (1u << FPL), "counter widths");
+__device__ __forceinline__ uint32_t vsum_by_index(uint32_t (&V)[VPL], uint32_t (&FC)[FPL], uint32_t sg) {
+    uint32_t qv = 0, qf = 0;
+#pragma unroll
+    for (int b = 0; b < VPL; ++b) {
+        qv += (1u << b) * idx_sum(V[b]);
+        V[b] = 0;
+    }
+#pragma unroll
+    for (int k = 0; k < FPL; ++k) {
+        qf += (1u << k) * idx_sum(FC[k]);
+        FC[k] = 0;
+    }
+    return 3 * qv + sg * qf; // mod 2^32: the sum itself is < 2^32
+}
+#else
 constexpr int FPL = ilog2c(VFLUSH + 1);     // VFLUSH < 2^FPL
 static_assert(VFLUSH * ((1u << NPL) - 1) < (1u << VPL) && VFLUSH < (1u << FPL), "counter widths");
-__device__ __forceinline__ uint32_t vsum_by_index(uint32_t (&V)[VPL], uint32_t (&FC)[FPL]) {
+__device__ __forceinline__ uint32_t vsum_by_index(uint32_t (&V)[VPL], uint32_t (&FC)[FPL], uint32_t) {
     uint32_t q = 0;
 #pragma unroll
     for (int b = 0; b < VPL; ++b) {
@@ -868,6 +889,33 @@ __device__ __forceinline__ uint32_t vsum_by_index(uint32_t (&V)[VPL], uint32_t (
         FC[k] = 0;
     }
     return q;
+}
+#endif
+
+// p of plane code c in class r
+__device__ __forceinline__ uint32_t code_p(uint32_t r, uint32_t c) {
+#if BS6_CODE
+    const uint32_t o = c & 1;
+    return r == 0 ? 3 * c + 1 + o : r == 2 ? 3 * c + 1 - o : 3 * c - 1 + o;
+#else
+    return 3 + 2 * c;
+#endif
+}
+
+// Per-class constants of the word sums (code mode): p = 3c + kf F + ke Z0.
+struct ClassSums {
+    uint32_t kz0;  // weight of popc(Z0) beyond 3: 3 + ke
+    uint32_t kf;   // weight of popc(F) (two's complement)
+    uint32_t g1m;  // g1 = Z0 & g1m
+    uint32_t sg;   // sign of the FC counter (two's complement)
+};
+__device__ __forceinline__ ClassSums class_sums(uint32_t r) {
+    ClassSums S;
+    S.kz0 = r == 2 ? 2u : 4u;
+    S.kf = r == 4 ? 0xFFFFFFFFu : 1u;
+    S.g1m = r == 0 ? ~0u : 0u;
+    S.sg = r == 4 ? 0xFFFFFFFFu : 1u;
+    return S;
 }
 
 // Bit-sliced scan of word w of class r: U in = valid evens of the word,
@@ -889,12 +937,20 @@ __device__ __forceinline__ void scan_word6(const uint32_t* tile, uint32_t r, uin
 template <bool PMIN>
 __device__ __forceinline__ void word_sums(const VerifyArgs& A, uint32_t w, uint32_t valid, uint32_t U,
                                           const uint32_t (&Z)[NPL], uint32_t ci, uint32_t delta, uint32_t i0,
-                                          uint32_t (&V)[VPL], uint32_t (&FC)[FPL], uint32_t& sp32, K3Acc& acc) {
+                                          uint32_t (&V)[VPL], uint32_t (&FC)[FPL], uint32_t& sp32, K3Acc& acc,
+                                          const ClassSums& CS, uint32_t r) {
     const uint32_t F = valid & ~U;
+#if BS6_CODE
+    // p = 3c + kf F + ke Z0: sum p of the word; il = ci + 3 (32w - delta + i)
+    uint32_t P = CS.kf * __popc(F) + CS.kz0 * __popc(Z[0]);
+#pragma unroll
+    for (int bp = 1; bp < NPL; ++bp) P += (3u << bp) * __popc(Z[bp]);
+#else
     // p = 3 + 2z: sum p of the word; il = ci + 3 (32w - delta + i)
     uint32_t P = 3 * __popc(F);
 #pragma unroll
     for (int bp = 0; bp < NPL; ++bp) P += (2u << bp) * __popc(Z[bp]);
+#endif
     sp32 += P;
     acc.spi += (uint64_t)P * (uint64_t)((int64_t)ci + 96 * (int64_t)w - 3 * (int64_t)delta);
     // V += Z, FC += F (ripple-carry, bit-sliced)
@@ -912,6 +968,24 @@ __device__ __forceinline__ void word_sums(const VerifyArgs& A, uint32_t w, uint3
         V[bp] = v ^ cy;
         cy = v & cy;
     }
+#if BS6_CODE
+    {
+        // FC += g0 + 2 g1 (g1 only in class 0)
+        const uint32_t g0 = F & ~Z[0], g1 = Z[0] & CS.g1m;
+        const uint32_t f0 = FC[0];
+        FC[0] = f0 ^ g0;
+        const uint32_t c0 = f0 & g0;
+        const uint32_t f1 = FC[1];
+        FC[1] = f1 ^ g1 ^ c0;
+        cy = (f1 & g1) | (c0 & (f1 ^ g1));
+#pragma unroll
+        for (int kk = 2; kk < FPL; ++kk) {
+            const uint32_t f = FC[kk];
+            FC[kk] = f ^ cy;
+            cy = f & cy;
+        }
+    }
+#else
     cy = F;
 #pragma unroll
     for (int kk = 0; kk < FPL; ++kk) {
@@ -919,13 +993,14 @@ __device__ __forceinline__ void word_sums(const VerifyArgs& A, uint32_t w, uint3
         FC[kk] = f ^ cy;
         cy = f & cy;
     }
+#endif
     if constexpr (PMIN) {
         for (uint32_t i = 0; i < 32; ++i) {
             if (!((F >> i) & 1)) continue;
             uint32_t z = 0;
 #pragma unroll
             for (int bp = 0; bp < NPL; ++bp) z |= ((Z[bp] >> i) & 1) << bp;
-            A.pmin_out[i0 + ci + 3 * (32 * w - delta + i)] = 3 + 2 * z;
+            A.pmin_out[i0 + ci + 3 * (32 * w - delta + i)] = code_p(r, z);
         }
     }
 }
@@ -1089,6 +1164,7 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
         uint32_t nbatch = 0; // batches in the vertical counters
         for (uint32_t ci = 0; ci < 3; ++ci) {
             const Class6 C = CL[ci];
+            const ClassSums CS = class_sums(C.r);
             const uint32_t T = ne > ci ? (ne - ci + 2) / 3 : 0;
             const uint32_t delta = C.G & 31;
             const uint32_t nw = (T + delta + 31) >> 5;
@@ -1103,17 +1179,24 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
                     uint32_t Z[NPL];
                     U = valid;
                     scan_word6(tile, C.r, w + (C.G >> 5), U, Z);
-                    word_sums<PMIN>(A, w, valid, U, Z, ci, delta, i0, V, FC, sp32, acc);
+                    word_sums<PMIN>(A, w, valid, U, Z, ci, delta, i0, V, FC, sp32, acc, CS, C.r);
                 }
                 if (++nbatch == VFLUSH) { // counters hold VFLUSH words
-                    acc.spi += 3ull * vsum_by_index(V, FC);
+                    acc.spi += 3ull * vsum_by_index(V, FC, CS.sg);
                     nbatch = 0;
                 }
                 qn = word_deep<PMIN>(tile, masks6, q, qn, U, w, ci, delta, C, lane, i0, s, J, CL, A, jlim_small, acc);
             }
+#if BS6_CODE
+            // the counters' weights are per class: flush at the class end
+            if (nbatch) {
+                acc.spi += 3ull * vsum_by_index(V, FC, CS.sg);
+                nbatch = 0;
+            }
+#endif
         }
         while (qn) qn = deep_round6<PMIN>(tile, masks6, q, qn, min(qn, 32u), lane, i0, s, J, CL, A, jlim_small, acc);
-        if (nbatch) acc.spi += 3ull * vsum_by_index(V, FC);
+        if (nbatch) acc.spi += 3ull * vsum_by_index(V, FC, 1u);
         acc.sp += sp32;
     } else {
         if (tid == 0) GB_STAT(6, 1);
@@ -1175,13 +1258,14 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
                     }
                 }
                 const uint32_t il = ci + 3 * (32 * w - delta + __ffs(cand) - 1);
-                if (bi == 0xFFFFFFFFu || mz > bz || (mz == bz && il < bi)) {
-                    bz = mz;
+                const uint32_t mp = code_p(C.r, mz); // codes are monotone in p within a class
+                if (bi == 0xFFFFFFFFu || mp > bz || (mp == bz && il < bi)) {
+                    bz = mp;
                     bi = il;
                 }
             }
         }
-        uint64_t kf = bi != 0xFFFFFFFFu ? (((uint64_t)(3 + 2 * bz) << 32) | (0xFFFFFFFFu - (i0 + bi))) : 0;
+        uint64_t kf = bi != 0xFFFFFFFFu ? (((uint64_t)bz << 32) | (0xFFFFFFFFu - (i0 + bi))) : 0;
         for (int o = 16; o; o >>= 1) {
             const uint64_t ok = __shfl_xor_sync(0xffffffffu, kf, o);
             kf = ok > kf ? ok : kf;

@@ -91,7 +91,34 @@ def scan6_words(pmax):
     return gmax // 32 + 2
 
 
-def gen_scan6(name, r, pmax, nplanes=None, nw=None, fma_every=0):
+def class_code(r, p, mode):
+    """Plane code of candidate p in class r.  mode "z": z = (p - 3)/2 (sum p =
+    3 + 2z).  mode "c": c ascends in smaller steps, so the plane intervals
+    are longer and fewer (fewer LOP3s per scan):
+      r = 0: p = 3c + 1 + (c & 1)            (5 -> 1, 7 -> 2, 11 -> 3, ...)
+      r = 2: p = 3 -> c = 1, p = 6y + 1 -> c = 2y   (p = 3c + 1 - (c & 1))
+      r = 4: p = 3 -> c = 1, p = 6y - 1 -> c = 2y   (p = 3c - 1 + (c & 1))
+    so p = 3c + kf F + ke Z0 with (kf, ke) = (1, 1), (1, -1), (-1, 1)."""
+    if mode == "z":
+        return (p - 3) // 2
+    if r == 0:
+        return (p - 1) // 3 if p % 6 == 1 else (p - 2) // 3
+    if p == 3:
+        return 1
+    return 2 * ((p - 1) // 6) if r == 2 else 2 * ((p + 1) // 6)
+
+
+def code_to_p(r, c, mode):
+    if mode == "z":
+        return 3 + 2 * c
+    if r == 0:
+        return 3 * c + 1 + (c & 1)
+    if r == 2:
+        return 3 * c + 1 - (c & 1)
+    return 3 * c - 1 + (c & 1)
+
+
+def gen_scan6(name, r, pmax, nplanes=None, nw=None, fma_every=0, mode="z"):
     """Wheel-6 scan for the words of evens n = r (mod 6).  The tile holds
     two arrays, A: q = Q + 6k (q = 1 mod 6) and B: q = Q + 4 + 6k (q = 5 mod 6);
     lane bit i of word w is class-r even t = 32w - delta + i, whose candidate
@@ -114,11 +141,15 @@ def gen_scan6(name, r, pmax, nplanes=None, nw=None, fma_every=0):
             cands.append((p, "a", (p - eps) // 6))
         elif q == 5:
             cands.append((p, "b", (p + 4 - eps) // 6))
-    zs = [(p - 3) // 2 for p, _, _ in cands]
+    zs = [class_code(r, p, mode) for p, _, _ in cands]
+    assert all(code_to_p(r, z, mode) == p for (p, _, _), z in zip(cands, zs))
+    assert zs == sorted(zs) and len(set(zs)) == len(zs)
     if nplanes is None:
-        nplanes = ((pmax - 3) // 2).bit_length()
+        nplanes = max(zs).bit_length()
+    assert max(zs) < (1 << nplanes)
     L = []
-    L.append(f"// class r = {r}: {len(cands)} candidates p <= {pmax}; planes Z[0..{nplanes - 1}] of z = (p - 3)/2")
+    what = "z = (p - 3)/2" if mode == "z" else "the class code c (class_code in tools/gen_bitslice.py)"
+    L.append(f"// class r = {r}: {len(cands)} candidates p <= {pmax}; planes Z[0..{nplanes - 1}] of {what}")
     if nw is None:
         nw = scan6_words(pmax)  # words per array: WB-(nw-1) .. WB
     args = ", ".join([f"uint32_t a{k}" for k in range(nw)] + [f"uint32_t b{k}" for k in range(nw)])
@@ -168,13 +199,15 @@ def main():
     ap.add_argument("--fma-every", type=int, default=0,
                     help="every N-th candidate's funnel shift on the FMA pipe (0: none)")
     ap.add_argument("--pbs-r24", type=int, default=449, help="classes 2/4 bound (0: --pbs6)")
+    ap.add_argument("--code", choices=["z", "c"], default="c",
+                    help="plane code: z = (p-3)/2, or the per-class code c (fewer plane intervals)")
     args = ap.parse_args()
     parts = []
-    parts.append(f"// gb_bitslice.cuh -- GENERATED by tools/gen_bitslice.py --shf-every {args.shf_every}; do not edit.")
+    parts.append(f"// gb_bitslice.cuh -- GENERATED by tools/gen_bitslice.py --code {args.code}; do not edit.")
     parts.append("//")
     parts.append("// Bit-sliced ascending candidate scan of the fused check (K3): one lane,")
     parts.append("// 32 consecutive evens, odd prime candidates in ascending order, the minimal")
-    parts.append("// p of each even recorded as z = (p - 3)/2 in bit planes.  Follows")
+    parts.append("// p of each even recorded as a monotone code of p in bit planes.  Follows")
     parts.append("// phase1_verify's scan order (reference proj/src/verifier.cpp:66-88).")
     parts.append("#pragma once")
     parts.append("#include <cstdint>")
@@ -194,10 +227,13 @@ def main():
     pr0 = args.pbs_r0 or args.pbs6
     pr24 = args.pbs_r24 or args.pbs6
     pmax = max(pr0, pr24)
-    npl = ((pmax - 3) // 2).bit_length()
+    npl = max(max(class_code(r, p, args.code) for p in odd_primes(pm) if p > 3 or r != 0)
+              for r, pm in ((0, pr0), (2, pr24), (4, pr24))).bit_length()
     nw = scan6_words(pmax)
+    parts.append(f"#define BS6_CODE {1 if args.code == 'c' else 0} // 1: planes hold the class code c, 0: z = (p - 3)/2")
     for r, pm in ((0, pr0), (2, pr24), (4, pr24)):
-        code, n, _, _ = gen_scan6(f"bs6_scan_r{r}", r, pm, nplanes=npl, nw=nw, fma_every=args.fma_every)
+        code, n, _, _ = gen_scan6(f"bs6_scan_r{r}", r, pm, nplanes=npl, nw=nw, fma_every=args.fma_every,
+                                  mode=args.code)
         parts.append("")
         parts.append(code)
     parts.append(f"constexpr uint32_t BS6_PMAX_R0 = {pr0};   // class 0 scans p <= BS6_PMAX_R0")
