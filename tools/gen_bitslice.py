@@ -198,7 +198,7 @@ def main():
     ap.add_argument("--pbs-r0", type=int, default=257, help="class-0 bound (0: --pbs6)")
     ap.add_argument("--fma-every", type=int, default=0,
                     help="every N-th candidate's funnel shift on the FMA pipe (0: none)")
-    ap.add_argument("--pbs-r24", type=int, default=449, help="classes 2/4 bound (0: --pbs6)")
+    ap.add_argument("--pbs-r24", type=int, default=503, help="classes 2/4 bound (0: --pbs6)")
     ap.add_argument("--code", choices=["z", "c"], default="c",
                     help="plane code: z = (p-3)/2, or the per-class code c (fewer plane intervals)")
     args = ap.parse_args()
