@@ -847,18 +847,22 @@ __device__ __forceinline__ uint32_t idx_sum(uint32_t x) {
 // sums of z (VPL planes), FC = per-position found counts (FPL planes);
 // p = 3 + 2z, so the sum is 2 sum_b 2^b idx(V_b) + 3 sum_k 2^k idx(FC_k).
 // Resets V and FC.
-#ifndef GB_VFLUSH
-#define GB_VFLUSH 8
+// words per vertical-counter reduction: longer batches amortise the flush
+// but widen the counters (registers); the check group's size decides
+#ifndef GB_VFLUSH_LIGHT
+#define GB_VFLUSH_LIGHT 16 // 16 check warps: one flush per class
 #endif
-constexpr uint32_t VFLUSH = GB_VFLUSH; // words per vertical-counter reduction
-constexpr int ilog2c(uint32_t x) { return x <= 1 ? 0 : 1 + ilog2c((x + 1) / 2); } // ceil(log2 x)
-constexpr int VPL = NPL + ilog2c(VFLUSH);   // VFLUSH * (2^NPL - 1) < 2^VPL
+#ifndef GB_VFLUSH_HEAVY
+#define GB_VFLUSH_HEAVY 8
+#endif
+__host__ __device__ constexpr int ilog2c(uint32_t x) { return x <= 1 ? 0 : 1 + ilog2c((x + 1) / 2); } // ceil(log2 x)
+__host__ __device__ constexpr int vpl_of(uint32_t vf) { return NPL + ilog2c(vf); } // vf (2^NPL - 1) < 2^vpl
 #if BS6_CODE
 // class code c: p = 3c + kf F + ke Z0 (gen_bitslice.py class_code), and
 // kf F + ke Z0 = sg (g0 + 2 g1) with g0 = F & ~Z0, g1 = Z0 (class 0) or 0,
 // sg = -1 for class 4, else +1.  FC counts g0 + 2 g1 per position.
-constexpr int FPL = ilog2c(2 * VFLUSH + 1); // 2 VFLUSH < 2^FPL
-static_assert(VFLUSH * ((1u << NPL) - 1) < (1u << VPL) && 2 * VFLUSH < (1u << FPL), "counter widths");
+__host__ __device__ constexpr int fpl_of(uint32_t vf) { return ilog2c(2 * vf + 1); } // 2 vf < 2^fpl
+template <int VPL, int FPL>
 __device__ __forceinline__ uint32_t vsum_by_index(uint32_t (&V)[VPL], uint32_t (&FC)[FPL], uint32_t sg) {
     uint32_t qv = 0, qf = 0;
 #pragma unroll
@@ -874,8 +878,8 @@ __device__ __forceinline__ uint32_t vsum_by_index(uint32_t (&V)[VPL], uint32_t (
     return 3 * qv + sg * qf; // mod 2^32: the sum itself is < 2^32
 }
 #else
-constexpr int FPL = ilog2c(VFLUSH + 1);     // VFLUSH < 2^FPL
-static_assert(VFLUSH * ((1u << NPL) - 1) < (1u << VPL) && VFLUSH < (1u << FPL), "counter widths");
+__host__ __device__ constexpr int fpl_of(uint32_t vf) { return ilog2c(vf + 1); } // vf < 2^fpl
+template <int VPL, int FPL>
 __device__ __forceinline__ uint32_t vsum_by_index(uint32_t (&V)[VPL], uint32_t (&FC)[FPL], uint32_t) {
     uint32_t q = 0;
 #pragma unroll
@@ -934,7 +938,7 @@ __device__ __forceinline__ void scan_word6(const uint32_t* tile, uint32_t r, uin
 
 // Sums of one scanned word: sum p (weighted by the word's even index), and
 // its z planes / found bits into the vertical counters.
-template <bool PMIN>
+template <bool PMIN, int VPL, int FPL>
 __device__ __forceinline__ void word_sums(const VerifyArgs& A, uint32_t w, uint32_t valid, uint32_t U,
                                           const uint32_t (&Z)[NPL], uint32_t ci, uint32_t delta, uint32_t i0,
                                           uint32_t (&V)[VPL], uint32_t (&FC)[FPL], uint32_t& sp32, K3Acc& acc,
@@ -1155,6 +1159,8 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
         // sum p * (bit index) is deferred: z planes and found bits of VFLUSH
         // words are summed per bit position as bit-sliced counters V (z) and
         // FC (found), then reduced by bit index once
+        constexpr uint32_t VFLUSH = GT >= 512 ? GB_VFLUSH_LIGHT : GB_VFLUSH_HEAVY;
+        constexpr int VPL = vpl_of(VFLUSH), FPL = fpl_of(VFLUSH);
         uint32_t V[VPL], FC[FPL];
 #pragma unroll
         for (int k = 0; k < VPL; ++k) V[k] = 0;
@@ -1179,7 +1185,7 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
                     uint32_t Z[NPL];
                     U = valid;
                     scan_word6(tile, C.r, w + (C.G >> 5), U, Z);
-                    word_sums<PMIN>(A, w, valid, U, Z, ci, delta, i0, V, FC, sp32, acc, CS, C.r);
+                    word_sums<PMIN, VPL, FPL>(A, w, valid, U, Z, ci, delta, i0, V, FC, sp32, acc, CS, C.r);
                 }
                 if (++nbatch == VFLUSH) { // counters hold VFLUSH words
                     acc.spi += 3ull * vsum_by_index(V, FC, CS.sg);
