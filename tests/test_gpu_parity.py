@@ -141,3 +141,30 @@ def test_c5_window_first_segments(gpu):
         tot_sum += got[r["a"]].as_dict()["sum_pmin"]
         tot_hash = (tot_hash + got[r["a"]].as_dict()["pos_hash"]) % (1 << 64)
     assert (tot_sum, tot_hash) == (g["sum_pmin"], g["pos_hash"])
+
+
+def test_c4_sampled_segments(gpu):
+    # C4 = [4, 1e13] is ~7 h of reference CPU time, so its records are
+    # pinned by sampling: every 500th segment and the
+    # last one, device (one batch stream at cover 1e13) vs the oracle
+    import os
+    from concurrent.futures import ThreadPoolExecutor
+
+    import oracle
+
+    limit, span = 10**13, 400_000_000
+    ks = list(range(0, 25_000, 500)) + [24_999]
+    segs = [(4 + k * span, min(4 + k * span + span - 2, limit)) for k in ks]
+    with gpu.Device(limit) as dev:
+        for a, b in segs:
+            dev.submit(a, b, tag=a)
+        got = {}
+        for _ in segs:
+            rec, tag = dev.wait()
+            got[tag] = rec.as_dict()
+    with ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        want = list(ex.map(lambda ab: oracle.verify_segment(ab[0], ab[1], cover=limit).as_dict(), segs))
+    for (a, b), w in zip(segs, want):
+        g = got[a]
+        for k in ("a", "b", "evens", "unverified", "phase2", "sum_pmin", "pos_hash", "max_p", "max_n", "n_ce"):
+            assert g[k] == w[k], (k, g, w)
