@@ -544,6 +544,9 @@ __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __re
     }
     q = pmc + nW + tid;
     qe = pmc + nB;
+#ifdef GB_SKIP_SINGLE // timing probe: no single-strike primes (wrong results)
+    qe = q;
+#endif
     for (; q + 7 * GT < qe; q += 8 * GT) {
         uint4 v[8];
 #pragma unroll
