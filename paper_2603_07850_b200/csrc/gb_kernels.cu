@@ -35,6 +35,10 @@ __device__ unsigned long long g_stats[8];
 #define GB_STAT(i, v) ((void)0)
 #endif
 
+#ifndef GB_PRED_STRIKE
+#define GB_PRED_STRIKE 1 // single-strike primes: predicated RED instead of a branch
+#endif
+
 // ============================================================ table init
 // Presieve patterns (odd-only for K1, wheel-6 for the fused kernel) and the
 // wheel-6 deep masks: masks6[c * NWIN6 + j] bit 63 - m set iff p = 6 g + off_c (g = 64 j
@@ -481,6 +485,20 @@ __device__ __forceinline__ void strike_warp6(uint32_t* arr, uint32_t o, uint32_t
     for (; wi < M6W; wi += p) atomicAnd(&arr[wi], mask);
 }
 
+// One strike if ok, without a branch: single-strike primes hit a block with
+// probability < 1/2, so a branch around the strike costs the warp its
+// BSSY/BRA/BSYNC on every site.  A miss ANDs ~0 into word `lane` instead (a
+// no-op; distinct banks across the warp), so the RED always issues.
+__device__ __forceinline__ void strike_if(uint32_t* arr, uint32_t c, bool ok, uint32_t lane) {
+#if GB_PRED_STRIKE
+    const uint32_t wi = ok ? (c >> 5) : lane;
+    const uint32_t m = ok ? __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, c) : ~0u;
+    atomicAnd(&arr[wi], m);
+#else
+    if (ok) strike(arr, c);
+#endif
+}
+
 // strikes c, c + step, ... < M6 of one class array (two per trip)
 __device__ __forceinline__ void strike_run6(uint32_t* arr, uint32_t c, uint32_t step) {
     while (c + step < M6) {
@@ -555,16 +573,16 @@ __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __re
         for (int u = 0; u < 8; ++u) {
             uint32_t oa, ob;
             block_off6(v[u], KB, oa, ob);
-            if (oa < M6) strike(A6, oa);
-            if (ob < M6) strike(B6, ob);
+            strike_if(A6, oa, oa < M6, lane);
+            strike_if(B6, ob, ob < M6, lane);
         }
     }
     for (; q < qe; q += GT) {
         const uint4 v = __ldg(q);
         uint32_t oa, ob;
         block_off6(v, KB, oa, ob);
-        if (oa < M6) strike(A6, oa);
-        if (ob < M6) strike(B6, ob);
+        strike_if(A6, oa, oa < M6, lane);
+        strike_if(B6, ob, ob < M6, lane);
     }
 }
 
