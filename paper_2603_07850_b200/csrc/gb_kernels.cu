@@ -500,13 +500,13 @@ __device__ __forceinline__ void strike_if(uint32_t* arr, uint32_t c, bool ok, ui
 }
 
 // strikes c, c + step, ... < M6 of one class array (two per trip)
-__device__ __forceinline__ void strike_run6(uint32_t* arr, uint32_t c, uint32_t step) {
+__device__ __forceinline__ void strike_run6(uint32_t* arr, uint32_t c, uint32_t step, uint32_t lane) {
     while (c + step < M6) {
         strike(arr, c);
         strike(arr, c + step);
         c += 2 * step;
     }
-    if (c < M6) strike(arr, c);
+    strike_if(arr, c, c < M6, lane);
 }
 
 // K2 strikes of one block by a group of GT threads (tid = index in the
@@ -549,16 +549,16 @@ __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __re
         for (int u = 0; u < 4; ++u) {
             uint32_t oa, ob;
             block_off6(v[u], KB, oa, ob);
-            strike_run6(A6, oa, v[u].x);
-            strike_run6(B6, ob, v[u].x);
+            strike_run6(A6, oa, v[u].x, lane);
+            strike_run6(B6, ob, v[u].x, lane);
         }
     }
     for (; q < qe; q += GT) {
         const uint4 v = __ldg(q);
         uint32_t oa, ob;
         block_off6(v, KB, oa, ob);
-        strike_run6(A6, oa, v.x);
-        strike_run6(B6, ob, v.x);
+        strike_run6(A6, oa, v.x, lane);
+        strike_run6(B6, ob, v.x, lane);
     }
     q = pmc + nW + tid;
     qe = pmc + nB;
