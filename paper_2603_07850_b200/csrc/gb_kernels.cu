@@ -35,6 +35,10 @@ __device__ unsigned long long g_stats[8];
 #define GB_STAT(i, v) ((void)0)
 #endif
 
+#ifndef GB_SS_INFLIGHT
+#define GB_SS_INFLIGHT 8 // single-strike rows loaded before their strikes
+#endif
+constexpr int SS_INFLIGHT = GB_SS_INFLIGHT;
 #ifndef GB_PRED_STRIKE
 #define GB_PRED_STRIKE 1 // single-strike primes: predicated RED instead of a branch
 #endif
@@ -565,12 +569,12 @@ __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __re
 #ifdef GB_SKIP_SINGLE // timing probe: no single-strike primes (wrong results)
     qe = q;
 #endif
-    for (; q + 7 * GT < qe; q += 8 * GT) {
-        uint4 v[8];
+    for (; q + (SS_INFLIGHT - 1) * GT < qe; q += SS_INFLIGHT * GT) {
+        uint4 v[SS_INFLIGHT];
 #pragma unroll
-        for (int u = 0; u < 8; ++u) v[u] = __ldg(q + u * GT);
+        for (int u = 0; u < SS_INFLIGHT; ++u) v[u] = __ldg(q + u * GT);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
+        for (int u = 0; u < SS_INFLIGHT; ++u) {
             uint32_t oa, ob;
             block_off6(v[u], KB, oa, ob);
             strike_if(A6, oa, oa < M6, lane);
