@@ -39,6 +39,9 @@ __device__ unsigned long long g_stats[8];
 #define GB_SS_INFLIGHT 8 // single-strike rows loaded before their strikes
 #endif
 constexpr int SS_INFLIGHT = GB_SS_INFLIGHT;
+#ifndef GB_RED_ADDR32
+#define GB_RED_ADDR32 1 // warp-cooperative strikes as REDs on 32-bit shared addresses
+#endif
 #ifndef GB_PRED_STRIKE
 #define GB_PRED_STRIKE 1 // single-strike primes: predicated RED instead of a branch
 #endif
@@ -478,6 +481,20 @@ __device__ __forceinline__ void strike_warp6(uint32_t* arr, uint32_t o, uint32_t
     const uint32_t c = o + lane * p;
     if (c >= M6) return;
     const uint32_t mask = __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, c);
+#if GB_RED_ADDR32
+    // 32-bit shared byte addresses, four REDs per trip off one pointer
+    const uint32_t base = (uint32_t)__cvta_generic_to_shared(arr);
+    const uint32_t end = base + 4 * M6W;
+    const uint32_t st = 4 * p; // bytes between strikes of this lane
+    uint32_t a = base + 4 * (c >> 5);
+    for (; a + 3 * st < end; a += 4 * st) {
+        asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(a), "r"(mask) : "memory");
+        asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(a + st), "r"(mask) : "memory");
+        asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(a + 2 * st), "r"(mask) : "memory");
+        asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(a + 3 * st), "r"(mask) : "memory");
+    }
+    for (; a < end; a += st) asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(a), "r"(mask) : "memory");
+#else
     uint32_t wi = c >> 5;
     const uint32_t p2 = 2 * p, p3 = 3 * p, p4 = 4 * p;
     for (; wi + p3 < M6W; wi += p4) {
@@ -487,6 +504,7 @@ __device__ __forceinline__ void strike_warp6(uint32_t* arr, uint32_t o, uint32_t
         atomicAnd(&arr[wi + p3], mask);
     }
     for (; wi < M6W; wi += p) atomicAnd(&arr[wi], mask);
+#endif
 }
 
 // One strike if ok, without a branch: single-strike primes hit a block with
