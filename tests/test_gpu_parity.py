@@ -168,3 +168,29 @@ def test_c4_sampled_segments(gpu):
         g = got[a]
         for k in ("a", "b", "evens", "unverified", "phase2", "sum_pmin", "pos_hash", "max_p", "max_n", "n_ce"):
             assert g[k] == w[k], (k, g, w)
+
+
+def test_ceiling_window_split_batch(gpu):
+    # the 2^64 ceiling window as 5 pieces in ONE batch, submitted out of
+    # order: base primes to 2^32 (k + p can pass 2^32 in the large-prime
+    # strikes), slots above / below slot 0; the merged totals equal the
+    # reference's one-segment record
+    r = golden("ceiling.json")["records"][0]
+    a, b = r["a"], r["b"]
+    cuts = [a, a + 20_000, a + 40_002, a + 60_000, a + 80_004, b + 2]
+    pieces = [(cuts[i], cuts[i + 1] - 2) for i in range(5)]
+    order = [2, 0, 4, 1, 3]
+    with gpu.Device(r["cover"], p_small=r["p_small"]) as dev:
+        for i in order:
+            dev.submit(*pieces[i], tag=i)
+        recs = [None] * 5
+        for _ in order:
+            rec, tag = dev.wait()
+            recs[tag] = rec.as_dict()
+    M = 1 << 64
+    assert sum(x["evens"] for x in recs) == r["evens"]
+    assert sum(x["unverified"] for x in recs) == 0 and sum(x["n_ce"] for x in recs) == 0
+    assert sum(x["sum_pmin"] for x in recs) % M == r["sum_pmin"]
+    assert sum(x["pos_hash"] for x in recs) % M == r["pos_hash"]
+    best = max(recs, key=lambda x: (x["max_p"], -x["max_n"]))
+    assert (best["max_p"], best["max_n"]) == (r["max_p"], r["max_n"])
