@@ -42,6 +42,9 @@ constexpr int SS_INFLIGHT = GB_SS_INFLIGHT;
 #ifndef GB_RED_ADDR32
 #define GB_RED_ADDR32 1 // warp-cooperative strikes as REDs on 32-bit shared addresses
 #endif
+#ifndef GB_CLASS_TEMPLATE
+#define GB_CLASS_TEMPLATE 1 // per-class scan + sums instantiated with immediate constants
+#endif
 #ifndef GB_PRED_STRIKE
 #define GB_PRED_STRIKE 1 // single-strike primes: predicated RED instead of a branch
 #endif
@@ -1052,6 +1055,29 @@ __device__ __forceinline__ void word_sums(const VerifyArgs& A, uint32_t w, uint3
     }
 }
 
+// Scan + sums of one word of class R (compile-time class: the per-class sum
+// constants become immediates).  Returns U (the deep evens).
+template <bool PMIN, uint32_t R, int VPL, int FPL>
+__device__ __forceinline__ uint32_t scan_sums(const VerifyArgs& A, const uint32_t* tile, uint32_t WB, uint32_t w,
+                                              uint32_t valid, uint32_t ci, uint32_t delta, uint32_t i0,
+                                              uint32_t (&V)[VPL], uint32_t (&FC)[FPL], uint32_t& sp32, K3Acc& acc) {
+    const uint32_t* a = arr_a(tile) + WB;
+    const uint32_t* b = arr_b(tile) + WB;
+    const uint32_t a0 = a[-3], a1 = a[-2], a2 = a[-1], a3 = a[0];
+    const uint32_t b0 = b[-3], b1 = b[-2], b2 = b[-1], b3 = b[0];
+    uint32_t U = valid, Z[NPL];
+    if constexpr (R == 0) bs6_scan_r0(a0, a1, a2, a3, b0, b1, b2, b3, U, Z);
+    else if constexpr (R == 2) bs6_scan_r2(a0, a1, a2, a3, b0, b1, b2, b3, U, Z);
+    else bs6_scan_r4(a0, a1, a2, a3, b0, b1, b2, b3, U, Z);
+    ClassSums CS;
+    CS.kz0 = R == 2 ? 2u : 4u;
+    CS.kf = R == 4 ? 0xFFFFFFFFu : 1u;
+    CS.g1m = R == 0 ? ~0u : 0u;
+    CS.sg = R == 4 ? 0xFFFFFFFFu : 1u;
+    word_sums<PMIN, VPL, FPL>(A, w, valid, U, Z, ci, delta, i0, V, FC, sp32, acc, CS, R);
+    return U;
+}
+
 // Deep evens of one word (U): appended to the warp's round queue, positions
 // from a ballot per count threshold (counts are 0..2 almost always); full
 // rounds run as soon as 32 entries wait.  Warp-uniform call.
@@ -1225,10 +1251,17 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
                 uint32_t U = 0;
                 if (w < nw) {
                     const uint32_t valid = (w == 0 || w + 1 == nw) ? word_mask6(w, T, delta) : ~0u;
-                    uint32_t Z[NPL];
                     U = valid;
+#if GB_CLASS_TEMPLATE
+                    // scan + sums with the class constants as immediates
+                    if (C.r == 0) U = scan_sums<PMIN, 0, VPL, FPL>(A, tile, w + (C.G >> 5), w, valid, ci, delta, i0, V, FC, sp32, acc);
+                    else if (C.r == 2) U = scan_sums<PMIN, 2, VPL, FPL>(A, tile, w + (C.G >> 5), w, valid, ci, delta, i0, V, FC, sp32, acc);
+                    else U = scan_sums<PMIN, 4, VPL, FPL>(A, tile, w + (C.G >> 5), w, valid, ci, delta, i0, V, FC, sp32, acc);
+#else
+                    uint32_t Z[NPL];
                     scan_word6(tile, C.r, w + (C.G >> 5), U, Z);
                     word_sums<PMIN, VPL, FPL>(A, w, valid, U, Z, ci, delta, i0, V, FC, sp32, acc, CS, C.r);
+#endif
                 }
                 if (++nbatch == VFLUSH) { // counters hold VFLUSH words
                     acc.spi += 3ull * vsum_by_index(V, FC, CS.sg);
