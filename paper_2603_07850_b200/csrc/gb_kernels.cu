@@ -369,9 +369,9 @@ __device__ __forceinline__ uint32_t first_a6(const SegJob& J, uint32_t p, uint64
     return (uint32_t)mod_magic(r * inv6_mod(p), p, m64);
 }
 
-// pmc[s*np + i] = {p, floor(2^32/p), p - 1 - k0, 4 6^-1 mod p} of tile prime
-// i (index iA0 + i), k0 = first_a6 at the slot's window origin; array B's
-// first index is k0 - 4 6^-1 (mod p).  Strikes start at the first multiple in
+// pmc[s*np + i] = {p, floor(2^32/p), k0 + p ceil(2^29/p), p - (4 6^-1 mod p)}
+// of tile prime i (index iA0 + i), k0 = first_a6 at the slot's window origin;
+// array B's first index is k0 - 4 6^-1 (mod p) (block_off6).  Strikes start at the first multiple in
 // the window, not at p^2: multiples below p^2 are composite anyway, and q = p
 // itself is restored by the low-window fix-up (fixup_low6).
 __global__ void k_segment_offsets(const SegJob* __restrict__ jobs, uint32_t nslots,
@@ -383,7 +383,8 @@ __global__ void k_segment_offsets(const SegJob* __restrict__ jobs, uint32_t nslo
     for (uint32_t i = blockIdx.x * blockDim.x + threadIdx.x; i < np; i += gridDim.x * blockDim.x) {
         const uint32_t p = primes[iA0 + i];
         const uint32_t k0 = first_a6(J, p, m64[iA0 + i]);
-        pmc[(size_t)s * np + i] = make_uint4(p, (uint32_t)((1ull << 32) / p), p - 1 - k0, b_shift6(p));
+        const uint32_t zk = k0 + p * (((1u << 29) + p - 1) / p); // < 2^29 + 2p
+        pmc[(size_t)s * np + i] = make_uint4(p, (uint32_t)((1ull << 32) / p), zk, p - b_shift6(p));
     }
 }
 
@@ -463,18 +464,19 @@ __device__ __forceinline__ uint32_t* arr_b(uint32_t* t) { return t + 2 * TPAD + 
 __device__ __forceinline__ const uint32_t* arr_a(const uint32_t* t) { return t + TPAD; }
 __device__ __forceinline__ const uint32_t* arr_b(const uint32_t* t) { return t + 2 * TPAD + M6W; }
 
-// Window cells of the first strikes of {p, m, d = p - 1 - k0, c} in arrays A
-// and B of the block starting at cell KB: (k0 - KB) mod p = p - 1 - ((KB + d)
-// mod p) by the magic m = floor(2^32/p) (quotient low by at most one), and
-// B's = A's - c (mod p).  Branch-free.
+// Window cells of the first strikes of {p, m, z, c'} in arrays A and B of
+// the block starting at cell KB: z = k0 + p ceil(2^29 / p) (so z - KB >= 0
+// for every block start), A's offset is (z - KB) mod p by the magic
+// m = floor(2^32/p) (quotient low by at most one), and B's is A's + c'
+// (mod p), c' = p - (4 6^-1 mod p).  Branch-free, two unsigned-min folds.
+static_assert((MAX_SEG_EVENS / E6 + 1) * (uint64_t)K6 < (1ull << 29), "block starts below 2^29 cells");
 __device__ __forceinline__ void block_off6(const uint4 v, uint32_t KB, uint32_t& oa, uint32_t& ob) {
     const uint32_t p = v.x;
-    const uint32_t y = KB + v.z;
-    uint32_t r = y - __umulhi(y, v.y) * p;
-    r = min(r, r - p);
-    oa = p - 1 - r;
-    const uint32_t t = oa - v.w;
-    ob = oa >= v.w ? t : t + p;
+    const uint32_t x = v.z - KB;
+    const uint32_t r = x - __umulhi(x, v.y) * p;
+    oa = min(r, r - p);
+    const uint32_t t = oa + v.w;
+    ob = min(t, t - p);
 }
 
 // Warp-cooperative strikes of one prime in one class array from cell o:
