@@ -81,7 +81,7 @@ constexpr uint32_t K6 = 260768;               // block stride in cells (32 * 814
 constexpr uint32_t E6 = 3 * K6;               // evens per block (782304)
 constexpr uint32_t PH6 = 8193;                // in-tile candidates p <= PH6
 constexpr int NWIN6 = 22;                     // 64-wide g-windows, g = p div 6 <= 1365
-constexpr uint32_t TPAD = 4;                  // zero words before / after each array (16-B aligned)
+constexpr uint32_t TPAD = 32;                 // zero words before / after each array (misses of branch-free strikes land here)
 constexpr uint32_t TILE6_WORDS = 3 * TPAD + 2 * M6W; // [pad][A][pad][B][pad]
 static_assert(K6 % 32 == 0 && 6 * (M6 - K6) > PH6 + 5, "wheel-6 block geometry");
 static_assert(64 * NWIN6 * 6 >= PH6, "deep windows cover the halo");

@@ -512,17 +512,17 @@ __device__ __forceinline__ void strike_warp6(uint32_t* arr, uint32_t o, uint32_t
 #endif
 }
 
-// One strike if ok, without a branch: single-strike primes hit a block with
-// probability < 1/2, so a branch around the strike costs the warp its
-// BSSY/BRA/BSYNC on every site.  A miss ANDs ~0 into word `lane` instead (a
-// no-op; distinct banks across the warp), so the RED always issues.
-__device__ __forceinline__ void strike_if(uint32_t* arr, uint32_t c, bool ok, uint32_t lane) {
+// One strike of cell c if c < M6, without a branch: single-strike primes hit a
+// block with probability < 1/2, so a branch around the strike costs the warp
+// its BSSY/BRA/BSYNC on every site.  A miss (c >= M6) is clamped into the
+// TPAD >= 32 zero words past the array (word M6W + lane at most; distinct
+// banks across the warp), where clearing a bit of a zero word is a no-op.
+static_assert(TPAD >= 32, "branch-free strikes need 32 pad words past each array");
+__device__ __forceinline__ void strike_if(uint32_t* arr, uint32_t c, uint32_t lane) {
 #if GB_PRED_STRIKE
-    const uint32_t wi = ok ? (c >> 5) : lane;
-    const uint32_t m = ok ? __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, c) : ~0u;
-    atomicAnd(&arr[wi], m);
+    strike(arr, min(c, M6 + 32 * lane));
 #else
-    if (ok) strike(arr, c);
+    if (c < M6) strike(arr, c);
 #endif
 }
 
@@ -533,7 +533,7 @@ __device__ __forceinline__ void strike_run6(uint32_t* arr, uint32_t c, uint32_t 
         strike(arr, c + step);
         c += 2 * step;
     }
-    strike_if(arr, c, c < M6, lane);
+    strike_if(arr, c, lane);
 }
 
 // K2 strikes of one block by a group of GT threads (tid = index in the
@@ -600,16 +600,16 @@ __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __re
         for (int u = 0; u < SS_INFLIGHT; ++u) {
             uint32_t oa, ob;
             block_off6(v[u], KB, oa, ob);
-            strike_if(A6, oa, oa < M6, lane);
-            strike_if(B6, ob, ob < M6, lane);
+            strike_if(A6, oa, lane);
+            strike_if(B6, ob, lane);
         }
     }
     for (; q < qe; q += GT) {
         const uint4 v = __ldg(q);
         uint32_t oa, ob;
         block_off6(v, KB, oa, ob);
-        strike_if(A6, oa, oa < M6, lane);
-        strike_if(B6, ob, ob < M6, lane);
+        strike_if(A6, oa, lane);
+        strike_if(B6, ob, lane);
     }
 }
 
