@@ -95,6 +95,7 @@ struct gb_dev {
     uint64_t sqrt_bound = 0, n_primes = 0;
     uint32_t* d_primes = nullptr;
     uint32_t iA0 = 0, iA1 = 0, iB1 = 0; // tile prime index ranges
+    uint32_t iQ1 = 0, iH1 = 0;          // first tile primes >= M6/4, >= M6/2
     uint32_t iW1 = 0;                   // first tile prime >= W
     uint16_t* d_wsplit = nullptr;       // [SPLIT_WARPS][32] balanced warp-cooperative primes
     uint32_t sw = WS_SW_LIGHT;          // sieve warps of the fused kernel
@@ -253,6 +254,8 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     A.iA0 = d->iA0;
     A.iA1 = d->iA1;
     A.iB1 = d->iB1;
+    A.iQ1 = d->iQ1;
+    A.iH1 = d->iH1;
     A.iW1 = d->iW1;
     A.np = np;
     A.sw = d->sw;
@@ -514,6 +517,8 @@ static int build_tables(gb_dev* d) {
     d->iA1 = (uint32_t)(std::lower_bound(hp.begin(), hp.end(), P_WARP_MAX) - hp.begin());
     d->iB1 = (uint32_t)(std::upper_bound(hp.begin(), hp.end(), P_TILE_MAX) - hp.begin());
     d->iW1 = std::max(d->iA1, std::min(d->iB1, (uint32_t)(std::lower_bound(hp.begin(), hp.end(), M6) - hp.begin())));
+    d->iQ1 = std::max(d->iA1, std::min(d->iW1, (uint32_t)(std::lower_bound(hp.begin(), hp.end(), M6 / 4) - hp.begin())));
+    d->iH1 = std::max(d->iQ1, std::min(d->iW1, (uint32_t)(std::lower_bound(hp.begin(), hp.end(), M6 / 2) - hp.begin())));
     d->iL0 = d->iB1;
     d->iL1 = total;
     {

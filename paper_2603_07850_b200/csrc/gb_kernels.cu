@@ -536,13 +536,44 @@ __device__ __forceinline__ void strike_run6(uint32_t* arr, uint32_t c, uint32_t 
     strike_if(arr, c, lane);
 }
 
+// Thread-per-prime strikes of rows [q, qe) (stride GT), INF rows loaded
+// before their strikes.  K = 0: runs of any length (strike_run6); K > 0: at
+// most K strikes per array, unrolled and clamped (strike_if).
+template <int GT, int K, int INF>
+__device__ __forceinline__ void strike_rows(uint32_t* A6, uint32_t* B6, const uint4* q, const uint4* qe, uint32_t KB,
+                                            uint32_t lane) {
+    auto one = [&](const uint4 v) {
+        uint32_t oa, ob;
+        block_off6(v, KB, oa, ob);
+        if constexpr (K == 0) {
+            strike_run6(A6, oa, v.x, lane);
+            strike_run6(B6, ob, v.x, lane);
+        } else {
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                strike_if(A6, oa + k * v.x, lane);
+                strike_if(B6, ob + k * v.x, lane);
+            }
+        }
+    };
+    for (; q + (INF - 1) * GT < qe; q += INF * GT) {
+        uint4 v[INF];
+#pragma unroll
+        for (int u = 0; u < INF; ++u) v[u] = __ldg(q + u * GT);
+#pragma unroll
+        for (int u = 0; u < INF; ++u) one(v[u]);
+    }
+    for (; q < qe; q += GT) one(__ldg(q));
+}
+
 // K2 strikes of one block by a group of GT threads (tid = index in the
 // group): warp-cooperative below P_WARP_MAX (rows wsplit[warp][..], balanced
 // by the host), one thread per prime above; primes >= M6 (index >= nW)
 // strike each array at most once.  pmc: this slot's rows (index i - iA0).
 template <int GT>
 __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __restrict__ pmc, uint32_t nA,
-                                               uint32_t nW, uint32_t nB, uint32_t KB, uint32_t tid,
+                                               uint32_t nQ, uint32_t nH, uint32_t nW, uint32_t nB, uint32_t KB,
+                                               uint32_t tid,
                                                const uint16_t* __restrict__ wsplit) {
     const uint32_t lane = tid & 31, warp = tid >> 5;
     uint32_t* A6 = arr_a(tile);
@@ -564,53 +595,15 @@ __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __re
             strike_warp6(B6, ob, p, lane);
         }
     }
-    // thread per prime; the rows come from L2, so 4 (8) loads are issued
-    // before their strikes to keep several in flight per warp
-    const uint4* q = pmc + nA + tid;
-    const uint4* qe = pmc + nW;
-    for (; q + 3 * GT < qe; q += 4 * GT) {
-        uint4 v[4];
-#pragma unroll
-        for (int u = 0; u < 4; ++u) v[u] = __ldg(q + u * GT);
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            uint32_t oa, ob;
-            block_off6(v[u], KB, oa, ob);
-            strike_run6(A6, oa, v[u].x, lane);
-            strike_run6(B6, ob, v[u].x, lane);
-        }
-    }
-    for (; q < qe; q += GT) {
-        const uint4 v = __ldg(q);
-        uint32_t oa, ob;
-        block_off6(v, KB, oa, ob);
-        strike_run6(A6, oa, v.x, lane);
-        strike_run6(B6, ob, v.x, lane);
-    }
-    q = pmc + nW + tid;
-    qe = pmc + nB;
-#ifdef GB_SKIP_SINGLE // timing probe: no single-strike primes (wrong results)
-    qe = q;
+    // thread per prime; the rows come from L2, so several are loaded before
+    // their strikes to keep loads in flight per warp.  Primes >= M6/4 strike
+    // an array at most 4 (>= M6/2: 2, >= M6: 1) times, unrolled branch-free.
+    strike_rows<GT, 0, 4>(A6, B6, pmc + nA + tid, pmc + nQ, KB, lane);
+    strike_rows<GT, 4, 4>(A6, B6, pmc + nQ + tid, pmc + nH, KB, lane);
+    strike_rows<GT, 2, SS_INFLIGHT>(A6, B6, pmc + nH + tid, pmc + nW, KB, lane);
+#ifndef GB_SKIP_SINGLE // timing probe: no single-strike primes (wrong results)
+    strike_rows<GT, 1, SS_INFLIGHT>(A6, B6, pmc + nW + tid, pmc + nB, KB, lane);
 #endif
-    for (; q + (SS_INFLIGHT - 1) * GT < qe; q += SS_INFLIGHT * GT) {
-        uint4 v[SS_INFLIGHT];
-#pragma unroll
-        for (int u = 0; u < SS_INFLIGHT; ++u) v[u] = __ldg(q + u * GT);
-#pragma unroll
-        for (int u = 0; u < SS_INFLIGHT; ++u) {
-            uint32_t oa, ob;
-            block_off6(v[u], KB, oa, ob);
-            strike_if(A6, oa, lane);
-            strike_if(B6, ob, lane);
-        }
-    }
-    for (; q < qe; q += GT) {
-        const uint4 v = __ldg(q);
-        uint32_t oa, ob;
-        block_off6(v, KB, oa, ob);
-        strike_if(A6, oa, lane);
-        strike_if(B6, ob, lane);
-    }
 }
 
 // Presieve one class array (M6W words) with the wheel-6 patterns; ph[g] =
@@ -1181,7 +1174,8 @@ __device__ __forceinline__ void sieve_block(const VerifyArgs& A, uint32_t* tile,
     presieve6(arr_b(tile), pat6, phb, tid, GT);
     gbar<GT>(bar);
 #ifndef GB_SKIP_STRIKES // timing probe: the check group on presieved-only tiles
-    strike_verify6<GT>(tile, A.pmc + (size_t)I.s * A.np, A.iA1 - A.iA0, A.iW1 - A.iA0, A.iB1 - A.iA0, I.KB, tid,
+    strike_verify6<GT>(tile, A.pmc + (size_t)I.s * A.np, A.iA1 - A.iA0, A.iQ1 - A.iA0, A.iH1 - A.iA0,
+                       A.iW1 - A.iA0, A.iB1 - A.iA0, I.KB, tid,
                        A.wsplit);
 #endif
     if (A.qg != nullptr && I.J.qg_words) {

@@ -29,6 +29,7 @@ struct VerifyArgs {
     uint64_t n_primes;
     uint64_t sbound;              // max(sqrt bound, 47): windows starting at or below need the fix-up
     uint32_t iA0, iA1, iB1;       // tile prime index ranges
+    uint32_t iQ1, iH1;            // first tile primes >= M6/4, >= M6/2 (at most 4 / 2 strikes per array)
     uint32_t iW1;                 // first tile prime >= M6 (strikes an array at most once)
     uint32_t np;                  // pmc row length (iB1 - iA0)
     uint32_t sw;                  // sieve warps of the kernel split (WS_SW_LIGHT / WS_SW_HEAVY)
