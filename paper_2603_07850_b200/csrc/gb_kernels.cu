@@ -35,10 +35,14 @@ __device__ unsigned long long g_stats[8];
 #define GB_STAT(i, v) ((void)0)
 #endif
 
-#ifndef GB_SS_INFLIGHT
-#define GB_SS_INFLIGHT 8 // single-strike rows loaded before their strikes
+// single-strike rows loaded before their strikes, by sieve-group size: the
+// light split (12 sieve warps) hides the L2 latency with more rows per warp
+#ifndef GB_SS_INFLIGHT_LIGHT
+#define GB_SS_INFLIGHT_LIGHT 16
 #endif
-constexpr int SS_INFLIGHT = GB_SS_INFLIGHT;
+#ifndef GB_SS_INFLIGHT_HEAVY
+#define GB_SS_INFLIGHT_HEAVY 12
+#endif
 #ifndef GB_RED_ADDR32
 #define GB_RED_ADDR32 1 // warp-cooperative strikes as REDs on 32-bit shared addresses
 #endif
@@ -600,6 +604,7 @@ __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __re
     // an array at most 4 (>= M6/2: 2, >= M6: 1) times, unrolled branch-free.
     strike_rows<GT, 0, 4>(A6, B6, pmc + nA + tid, pmc + nQ, KB, lane);
     strike_rows<GT, 4, 4>(A6, B6, pmc + nQ + tid, pmc + nH, KB, lane);
+    constexpr int SS_INFLIGHT = GT == 32 * WS_SW_LIGHT ? GB_SS_INFLIGHT_LIGHT : GB_SS_INFLIGHT_HEAVY;
     strike_rows<GT, 2, SS_INFLIGHT>(A6, B6, pmc + nH + tid, pmc + nW, KB, lane);
 #ifndef GB_SKIP_SINGLE // timing probe: no single-strike primes (wrong results)
     strike_rows<GT, 1, SS_INFLIGHT>(A6, B6, pmc + nW + tid, pmc + nB, KB, lane);
