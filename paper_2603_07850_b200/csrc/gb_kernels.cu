@@ -37,6 +37,9 @@ __device__ unsigned long long g_stats[8];
 
 // single-strike rows loaded before their strikes, by sieve-group size: the
 // light split (12 sieve warps) hides the L2 latency with more rows per warp
+#ifndef GB_RUN_INFLIGHT
+#define GB_RUN_INFLIGHT 4 // run-prime rows loaded before their strikes
+#endif
 #ifndef GB_SS_INFLIGHT_LIGHT
 #define GB_SS_INFLIGHT_LIGHT 16
 #endif
@@ -602,8 +605,8 @@ __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __re
     // thread per prime; the rows come from L2, so several are loaded before
     // their strikes to keep loads in flight per warp.  Primes >= M6/4 strike
     // an array at most 4 (>= M6/2: 2, >= M6: 1) times, unrolled branch-free.
-    strike_rows<GT, 0, 4>(A6, B6, pmc + nA + tid, pmc + nQ, KB, lane);
-    strike_rows<GT, 4, 4>(A6, B6, pmc + nQ + tid, pmc + nH, KB, lane);
+    strike_rows<GT, 0, GB_RUN_INFLIGHT>(A6, B6, pmc + nA + tid, pmc + nQ, KB, lane);
+    strike_rows<GT, 4, GB_RUN_INFLIGHT>(A6, B6, pmc + nQ + tid, pmc + nH, KB, lane);
     constexpr int SS_INFLIGHT = GT == 32 * WS_SW_LIGHT ? GB_SS_INFLIGHT_LIGHT : GB_SS_INFLIGHT_HEAVY;
     strike_rows<GT, 2, SS_INFLIGHT>(A6, B6, pmc + nH + tid, pmc + nW, KB, lane);
 #ifndef GB_SKIP_SINGLE // timing probe: no single-strike primes (wrong results)
