@@ -28,7 +28,7 @@ using namespace gbk;
 namespace {
 
 constexpr int NBATCH = 3;                 // batches in flight per device
-constexpr uint32_t SLOTS = 8;             // pieces per batch
+constexpr uint32_t SLOTS = MAX_SLOTS;     // pieces per batch
 constexpr uint32_t LIST_CAP = 1u << 20;   // straggler entries per batch
 constexpr uint64_t MAX_PIECE = MAX_SEG_EVENS; // cells of a piece stay < 2^31 - 1 (block_off)
 

@@ -45,6 +45,7 @@ constexpr uint32_t P_TILE_MAX = 1u << 22; // base primes above: K_large (global 
 constexpr uint32_t P_WARP_MAX = GB_P_WARP_MAX; // primes below: warp-cooperative strikes
 constexpr uint32_t FIRST_STRIKE_P = 53;   // primes below are in the presieve patterns
 constexpr uint32_t MAX_SEG_EVENS = 1u << 30; // device sub-segment (piece) limit
+constexpr uint32_t MAX_SLOTS = 8;             // pieces (slots) per batch launch
 
 // presieve pattern groups (products of small odd primes); pattern bit k is 0
 // iff 2k+1 is divisible by a prime of the group.  Stored with wrap-around

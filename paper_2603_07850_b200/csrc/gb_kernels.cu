@@ -1145,12 +1145,12 @@ struct BlockInfo {
     int64_t Qs;     // window origin (valid when low)
 };
 
-__device__ __forceinline__ BlockInfo block_info(const VerifyArgs& A, uint32_t fb) {
+__device__ __forceinline__ BlockInfo block_info(const VerifyArgs& A, const SegJob* jobs, uint32_t fb) {
     BlockInfo I;
     uint32_t s = 0; // few slots: linear scan
-    while (s + 1 < A.nslots && A.jobs[s + 1].block_prefix <= fb) ++s;
+    while (s + 1 < A.nslots && jobs[s + 1].block_prefix <= fb) ++s;
     I.s = s;
-    I.J = A.jobs[s];
+    I.J = jobs[s];
     I.b = fb - I.J.block_prefix;
     I.KB = I.b * K6;
     const uint64_t off = 6ull * I.KB;
@@ -1386,6 +1386,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
 
     for (uint32_t i = threadIdx.x; i < PAT6_WORDS; i += blockDim.x) pat6[i] = A.gpat6[i];
     for (uint32_t i = threadIdx.x; i < 3u * NWIN6; i += blockDim.x) masks6[i] = A.masks6[i];
+    // the batch's jobs (block lookup at every block start reads them)
+    __shared__ SegJob s_jobs[MAX_SLOTS];
+    static_assert(sizeof(SegJob) % 4 == 0, "word copy");
+    for (uint32_t i = threadIdx.x; i < A.nslots * (uint32_t)(sizeof(SegJob) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t*>(s_jobs)[i] = reinterpret_cast<const uint32_t*>(A.jobs)[i];
     for (uint32_t i = threadIdx.x; i < 2 * TILE6_WORDS; i += blockDim.x) tiles[i] = 0; // pads stay zero
     __syncthreads();
     const int NB = WS_THREADS; // participants of FULL / EMPTY
@@ -1407,7 +1412,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
                 return;
             }
             if (tid == 0) fb_next = atomicAdd(A.block_counter, 1u);
-            const BlockInfo I = block_info(A, fb);
+            const BlockInfo I = block_info(A, s_jobs, fb);
             sieve_block<ST>(A, tile, pat6, I, tid, BAR_S);
             nb_arrive(BAR_FULL + bs, NB);
         }
@@ -1419,7 +1424,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
             nb_sync(BAR_FULL + bs, NB);
             const uint32_t fb = s_fb[bs];
             if (fb >= A.total_blocks) return;
-            const BlockInfo I = block_info(A, fb);
+            const BlockInfo I = block_info(A, s_jobs, fb);
 #ifndef GB_SKIP_CHECK // timing probe: sieve group alone
             check_block<PMIN, CT>(A, tiles + bs * TILE6_WORDS, masks6, I, tid, BAR_C, s_red, &s_key, s_q);
 #endif
@@ -1678,6 +1683,7 @@ cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint3
     return cudaGetLastError();
 }
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st) {
+    if (a.nslots > MAX_SLOTS) return cudaErrorInvalidValue; // s_jobs holds MAX_SLOTS
     // the sieve/check split follows the sieve's share of the work, which
     // grows with the number of tile primes (a.sw, chosen by the host)
     if (a.sw == WS_SW_HEAVY) {
