@@ -1208,14 +1208,11 @@ __device__ __forceinline__ void sieve_block(const VerifyArgs& A, uint32_t* tile,
 // the block's sums / max key go to the slot accumulators.
 template <bool PMIN, int GT>
 __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t* tile, const uint64_t* masks6,
-                                            const BlockInfo& I, uint32_t tid, int bar,
-                                            unsigned long long (*s_red)[3], unsigned long long* s_key_p,
-                                            uint32_t (*s_q)[QCAP]) {
+                                            const BlockInfo& I, uint32_t tid, uint32_t (*s_q)[QCAP]) {
     const uint32_t lane = tid & 31, warp = tid >> 5;
     const uint32_t jlim_small = A.p_small >= 3 ? (uint32_t)min((A.p_small - 3) / 2, (uint64_t)0xFFFFFFFFu) : 0;
     const uint32_t s = I.s;
     const SegJob& J = I.J;
-    unsigned long long& s_key = *s_key_p;
     const uint32_t i0 = I.b * E6;
     const uint32_t ne = min(E6, J.evens - i0);
     const uint64_t n_first = J.a + 2ull * i0, n_last = n_first + 2ull * (ne - 1);
@@ -1291,7 +1288,9 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
         for (uint32_t il = tid; il < ne; il += GT) generic_even6<PMIN>(tile, masks6, il, i0, s, J, A, jlim_small, acc);
 #endif
     }
-    // ---- block reduction -> slot accumulators; key = p << 32 | ~iseg
+    // ---- per-warp reduction -> slot accumulators; key = p << 32 | ~iseg.
+    // No block barrier: sums are added per warp, and the max is taken per
+    // warp (global atomicMax), so a warp never waits for the others.
     uint64_t key = acc.mp ? (((uint64_t)acc.mp << 32) | (0xFFFFFFFFu - (i0 + acc.mi))) : 0;
     uint64_t sp64 = acc.sp, spi = acc.spi + (uint64_t)i0 * acc.sp;
     for (int o = 16; o; o >>= 1) {
@@ -1300,28 +1299,10 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
         const uint64_t ok = __shfl_xor_sync(0xffffffffu, key, o);
         key = ok > key ? ok : key;
     }
-    if (lane == 0) {
-        s_red[warp][0] = sp64;
-        s_red[warp][1] = spi;
-        s_red[warp][2] = key;
-    }
-    gbar<GT>(bar);
-    if (tid == 0) {
-        uint64_t S = 0, SPI = 0, K = 0;
-        for (int w = 0; w < GT / 32; ++w) {
-            S += s_red[w][0];
-            SPI += s_red[w][1];
-            K = s_red[w][2] > K ? s_red[w][2] : K;
-        }
-        atomicAdd(&A.acc[s].sum, (unsigned long long)S);
-        atomicAdd(&A.acc[s].hash, (unsigned long long)((J.a >> 1) * S + SPI));
-        s_key = K;
-    }
-    gbar<GT>(bar);
-    uint64_t K = s_key;
-    if (fast && K < ((uint64_t)(PBS + 2) << 32)) {
-        // no deep even beat the bit-sliced range: the block max may be a
-        // bit-sliced even -- rescan for max z (smallest il on ties)
+    if (fast && key < ((uint64_t)(PBS + 2) << 32)) {
+        // no deep even of this warp beat the bit-sliced range: its max may be
+        // a bit-sliced even -- rescan its own words (w = tid mod GT, as in the
+        // fast loop) for the max code (smallest il on ties)
         uint32_t bz = 0, bi = 0xFFFFFFFFu;
         for (uint32_t ci = 0; ci < 3; ++ci) {
             const Class6 C = class6(J, ci);
@@ -1356,11 +1337,13 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
             const uint64_t ok = __shfl_xor_sync(0xffffffffu, kf, o);
             kf = ok > kf ? ok : kf;
         }
-        if (lane == 0) atomicMax(&s_key, (unsigned long long)kf);
-        gbar<GT>(bar);
-        K = s_key;
+        key = kf > key ? kf : key;
     }
-    if (tid == 0 && K) atomicMax(&A.acc[s].key, (unsigned long long)K);
+    if (lane == 0) {
+        atomicAdd(&A.acc[s].sum, (unsigned long long)sp64);
+        atomicAdd(&A.acc[s].hash, (unsigned long long)((J.a >> 1) * sp64 + spi));
+        if (key) atomicMax(&A.acc[s].key, (unsigned long long)key);
+    }
 }
 
 // Warp-specialised fused kernel: one 896-thread CTA per SM, two wheel-6
@@ -1370,7 +1353,7 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
 // FULL[b] (sieve arrives, check waits) and EMPTY[b] (check arrives, sieve
 // waits), so the atomic-heavy sieve and the ALU-heavy check overlap instead
 // of alternating at CTA barriers.
-constexpr int BAR_S = 1, BAR_C = 2, BAR_FULL = 3, BAR_EMPTY = 5; // FULL/EMPTY + buffer
+constexpr int BAR_S = 1, BAR_FULL = 3, BAR_EMPTY = 5; // FULL/EMPTY + buffer (the check group has no internal barrier)
 
 template <bool PMIN, int SW>
 __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
@@ -1380,8 +1363,6 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
     uint32_t* pat6 = smem + WS_PAT_OFF;                     // PAT6_WORDS
     uint64_t* masks6 = (uint64_t*)(smem + WS_MASK_OFF);     // 3 x NWIN6
     __shared__ uint32_t s_fb[2];
-    __shared__ unsigned long long s_red[CT / 32][3];
-    __shared__ unsigned long long s_key;
     __shared__ uint32_t s_q[CT / 32][QCAP];
 
     for (uint32_t i = threadIdx.x; i < PAT6_WORDS; i += blockDim.x) pat6[i] = A.gpat6[i];
@@ -1426,7 +1407,7 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
             if (fb >= A.total_blocks) return;
             const BlockInfo I = block_info(A, s_jobs, fb);
 #ifndef GB_SKIP_CHECK // timing probe: sieve group alone
-            check_block<PMIN, CT>(A, tiles + bs * TILE6_WORDS, masks6, I, tid, BAR_C, s_red, &s_key, s_q);
+            check_block<PMIN, CT>(A, tiles + bs * TILE6_WORDS, masks6, I, tid, s_q);
 #endif
             nb_arrive(BAR_EMPTY + bs, NB);
         }
