@@ -899,10 +899,10 @@ __device__ __forceinline__ uint32_t idx_sum(uint32_t x) {
 // words per vertical-counter reduction: longer batches amortise the flush
 // but widen the counters (registers); the check group's size decides
 #ifndef GB_VFLUSH_LIGHT
-#define GB_VFLUSH_LIGHT 16 // 16 check warps: one flush per class
+#define GB_VFLUSH_LIGHT 16 // 16 check warps: 16 steps per class, one flush
 #endif
 #ifndef GB_VFLUSH_HEAVY
-#define GB_VFLUSH_HEAVY 12 // 12 check warps: two flushes per class
+#define GB_VFLUSH_HEAVY 22 // 12 check warps: 22 steps per class, one flush
 #endif
 __host__ __device__ constexpr int ilog2c(uint32_t x) { return x <= 1 ? 0 : 1 + ilog2c((x + 1) / 2); } // ceil(log2 x)
 __host__ __device__ constexpr int vpl_of(uint32_t vf) { return NPL + ilog2c(vf); } // vf (2^NPL - 1) < 2^vpl
