@@ -52,11 +52,19 @@ int gb_pool_create(uint64_t start, uint64_t limit, uint64_t seg_size,
 /* claim_next (pool.cpp:24-31): 1 and the job, 0 when exhausted, <0 = -status. */
 int gb_pool_claim(gb_pool* pool, uint64_t* a, uint64_t* b, uint64_t* index);
 
+/* Cooperative stop (pool.cpp:104-111): after gb_pool_request_stop every
+ * claim on this pool -- in every process attached to a shared cursor --
+ * returns 0.  Workers set it when a segment has counterexamples.
+ * gb_pool_stop_requested returns 1 once set. */
+int gb_pool_request_stop(gb_pool* pool);
+int gb_pool_stop_requested(const gb_pool* pool);
+
 /* Frees the handle; unlink=1 also removes the shared-memory object. */
 int gb_pool_destroy(gb_pool* pool, int unlink);
 
 /* One GPU worker (pool.cpp:90-120) on an open device: claims segments until
- * the pool is exhausted (or a counterexample is found), keeps up to
+ * the pool is exhausted or stopped (a counterexample here sets the pool's
+ * stop, which every attached rank honours), keeps up to
  * max_inflight segments in flight (0 = device maximum; slow start from 1),
  * and returns this worker's merged result. */
 int gb_drain_pool(gb_dev* dev, gb_pool* pool, int max_inflight, gb_run_result* out);

@@ -103,6 +103,8 @@ def ref():
         L.ref_phase2_resolve.argtypes = [u64, u64, p64]; L.ref_phase2_resolve.restype = C.c_int
         L.ref_segment_record.argtypes = [u64, u64, u64, u64, u64, C.POINTER(SegRecord)]
         L.ref_segment_record.restype = C.c_int
+        L.ref_segment_record1.argtypes = [u64, u64, u64, u64, u64, C.POINTER(SegRecord)]
+        L.ref_segment_record1.restype = C.c_int
         _ref = L
     return _ref
 
@@ -211,6 +213,18 @@ def ref_segment_record(a: int, b: int, cover: int | None = None, p_small: int = 
                                   inject_fail, C.byref(rec))
     if rc:
         raise ValueError(f"ref_segment_record rc={rc}")
+    return rec
+
+
+def ref_segment_record1(a: int, b: int, cover: int | None = None, p_small: int = 1_000_000,
+                        inject_fail: int = 0) -> SegRecord:
+    """Single-pass reference record (same reference functions, same order as
+    verify_segment; see oracle/ref_shim.cpp ref_segment_record1)."""
+    rec = SegRecord()
+    rc = ref().ref_segment_record1(a, b, cover if cover is not None else b, p_small,
+                                   inject_fail, C.byref(rec))
+    if rc:
+        raise ValueError(f"ref_segment_record1 rc={rc}")
     return rec
 
 

@@ -153,4 +153,55 @@ int ref_segment_record(uint64_t a, uint64_t b, uint64_t cover, uint64_t p_small,
     }
 }
 
+// Single-pass form of ref_segment_record for the large golden sets (C4/C5).
+// Composes the same reference functions in the same order as verify_segment
+// (verifier.cpp:172-200): sieve_range_for -> tiled_sieve_segment ->
+// phase1_verify (with min_primes_out, so the checksum needs no second pass)
+// -> inject clear -> count_unverified -> phase2_resolve per leftover.
+// Cross-checked against ref_segment_record (which calls verify_segment
+// itself) by make_big_goldens.py --selfcheck.
+int ref_segment_record1(uint64_t a, uint64_t b, uint64_t cover, uint64_t p_small,
+                        uint64_t inject, gb_seg_record* rec) {
+    try {
+        Tables& t = tables(cover, p_small);
+        std::memset(rec, 0, sizeof(*rec));
+        rec->a = a;
+        rec->b = b;
+        SegmentJob job{a, b, 0};
+        OddRange r = sieve_range_for(job, p_small);
+        OddBitset q = tiled_sieve_segment(r.lo, r.hi, t.base);
+        std::vector<uint64_t> mp;
+        Phase1Result p1 = phase1_verify(job, t.small, q, 2'000'000, &mp);
+        MinPrimeMax mpm = p1.min_prime;
+        rec->evens_checked = p1.verified.size();
+        gb_seg_record chk{};
+        for (size_t i = 0; i < mp.size(); ++i)
+            if (mp[i]) observe(&chk, mp[i], a + 2 * i);
+        if (inject >= a && inject <= b && (inject & 1) == 0)
+            p1.verified.clear((inject - a) >> 1);
+        UnverifiedSet left = count_unverified(p1.verified, a);
+        rec->unverified_p1 = left.count;
+        std::vector<uint64_t> ces;
+        for (uint64_t n : left.values) {
+            if (n == inject) { ces.push_back(n); continue; }
+            auto hit = phase2_resolve(n, t.small, t.phase2);
+            if (!hit) { ces.push_back(n); continue; }
+            ++rec->phase2_resolved;
+            mpm.observe(hit->p, n);
+            observe(&chk, hit->p, n);
+        }
+        rec->n_counterexamples = ces.size();
+        for (size_t i = 0; i < ces.size() && i < GB_REC_MAX_CE; ++i)
+            rec->counterexamples[i] = ces[i];
+        rec->pmin_sum = chk.pmin_sum;
+        rec->pmin_hash = chk.pmin_hash;
+        rec->max_p = mpm.p;
+        rec->max_n = mpm.n;
+        if (chk.max_p != mpm.p || chk.max_n != mpm.n) return -3;
+        return 0;
+    } catch (...) {
+        return -1;
+    }
+}
+
 } // extern "C"

@@ -21,8 +21,17 @@ __all__ = [
 ]
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-# GB_LIB_PATH: load a differently built copy (tools/variants.sh timing runs)
-LIB_PATH = os.environ.get("GB_LIB_PATH") or os.path.join(HERE, "libgoldbach_b200.so")
+DEFAULT_LIB_PATH = os.path.join(HERE, "libgoldbach_b200.so")
+# Tools-only switch: tools/variants.sh timing runs load a differently built
+# copy with GB_LIB_PATH, honoured only together with GB_TOOLS_LIB_OVERRIDE=1
+# so a stray environment variable cannot swap the product library.
+_override = os.environ.get("GB_LIB_PATH")
+if _override and os.environ.get("GB_TOOLS_LIB_OVERRIDE") == "1":
+    import sys as _sys
+    print(f"paper_2603_07850_b200: tools override, loading {_override}", file=_sys.stderr)
+    LIB_PATH = _override
+else:
+    LIB_PATH = DEFAULT_LIB_PATH
 CLI_PATH = os.path.join(HERE, "bin", "goldbach")
 GB_REC_MAX_CE = 16
 
@@ -164,6 +173,8 @@ def _bind_pool(L):
         "gb_pool_create": ([u64, u64, u64, C.c_char_p, i32, C.POINTER(vp)], i32),
         "gb_pool_claim": ([vp, p64, p64, p64], i32),
         "gb_pool_destroy": ([vp, i32], i32),
+        "gb_pool_request_stop": ([vp], i32),
+        "gb_pool_stop_requested": ([vp], i32),
         "gb_drain_pool": ([vp, vp, i32, C.POINTER(RunResult)], i32),
         "gb_run_range": ([u64, u64, u64, u64, u64, C.POINTER(i32), i32, i32, i32,
                           C.POINTER(RunResult), p64], i32),
@@ -374,6 +385,15 @@ class Pool:
             raise _ERRS.get(-rc, GoldbachError)("gb_pool_claim failed")
         return (a.value, b.value, i.value) if rc == 1 else None
 
+    def request_stop(self):
+        """Cooperative stop (pool.cpp:104-111): later claims on this pool,
+        in every process attached to the shared cursor, return None."""
+        _check_pool(lib().gb_pool_request_stop(self._h))
+
+    @property
+    def stop_requested(self) -> bool:
+        return bool(lib().gb_pool_stop_requested(self._h))
+
     def close(self, unlink: Optional[bool] = None):
         if getattr(self, "_h", None):
             lib().gb_pool_destroy(self._h, 1 if (self.owner if unlink is None else unlink) else 0)
@@ -388,6 +408,11 @@ class Pool:
     @property
     def handle(self):
         return self._h
+
+
+def _check_pool(rc: int):
+    if rc:
+        raise _ERRS.get(rc, GoldbachError)(lib().gb_pool_last_error().decode(errors="replace"))
 
 
 def estimate_device_bytes(cover_limit: int, p_small: int = 1_000_000,
@@ -409,9 +434,12 @@ def run_range(start: int, limit: int, seg_size: int = 200_000_000, p_small: int 
     `devices` round-robin: returns (RunResult, per_worker_segments)."""
     devs = list(devices)
     k = workers if workers is not None else len(devs)
+    # the worker count exactly as gb_run_range computes it (pool_capi.cpp),
+    # so per_worker_segments is sized for every entry the C side writes
+    k = k if k and k > 0 else max(1, len(devs))
     arr = (C.c_int * len(devs))(*devs)
     res = RunResult()
-    per = (C.c_uint64 * max(k, 1))()
+    per = (C.c_uint64 * k)()
     rc = lib().gb_run_range(start, limit, seg_size, p_small, inject_fail, arr, len(devs), k,
                             1 if progress else 0, C.byref(res), per)
     if rc:

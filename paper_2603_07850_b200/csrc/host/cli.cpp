@@ -103,6 +103,7 @@ void print_json(std::ostream& out, const Config& cfg, unsigned workers, const Ru
     j.put("pmin_hash", r.pmin_hash);
     j.put_list("gpus", r.worker_devices);
     j.put("init_seconds", r.init_seconds);
+    j.put("counterexample_count", r.counterexample_count);
     out << j.str() << "\n";
 }
 
@@ -237,22 +238,28 @@ MemoryEstimate validate_resources(const Config& cfg) {
     est.per_worker_bytes = gb_estimate_device_bytes(cfg.limit, cfg.p_small, cfg.seg_size);
     est.shared_bytes = 1 << 20; // host-side records and pinned staging
     est.total_bytes = est.per_worker_bytes * est.workers + est.shared_bytes;
-    // workers share GPUs round-robin: the most loaded GPU holds ceil(k / g)
+    // workers are mapped round-robin onto every visible GPU (run_workers'
+    // worker_devices): check each device's load against that device's own
+    // budget, before any worker is spawned (cli.cpp:264-296)
     const unsigned gpus = (unsigned)std::max(1, visible_gpus());
-    const uint64_t per_gpu = est.per_worker_bytes * ((est.workers + gpus - 1) / gpus);
-    uint64_t budget = 0;
-    std::string what;
-    if (cfg.mem_cap) {
-        budget = *cfg.mem_cap;
-        what = "--mem-cap ";
-    } else {
-        uint64_t fr = 0, tot = 0;
-        budget = gb_device_memory(0, &fr, &tot) == GB_OK ? fr : ~uint64_t{0};
-        what = "free GPU memory ";
+    for (unsigned g = 0; g < gpus && g < est.workers; ++g) {
+        const uint64_t on_g = est.workers / gpus + (g < est.workers % gpus ? 1 : 0);
+        const uint64_t load = est.per_worker_bytes * on_g;
+        uint64_t budget = 0;
+        std::string what;
+        if (cfg.mem_cap) {
+            budget = *cfg.mem_cap;
+            what = "--mem-cap ";
+        } else {
+            uint64_t fr = 0, tot = 0;
+            budget = gb_device_memory((int)g, &fr, &tot) == GB_OK ? fr : ~uint64_t{0};
+            what = "free memory of GPU " + std::to_string(g) + " ";
+        }
+        if (load > budget)
+            throw ResourceError("estimated footprint " + human_bytes(load) + " of GPU " + std::to_string(g) + " (" +
+                                std::to_string(on_g) + " worker(s)) exceeds " + what + human_bytes(budget) +
+                                " (reduce --seg-size or --gpus)");
     }
-    if (per_gpu > budget)
-        throw ResourceError("estimated per-GPU footprint " + human_bytes(per_gpu) + " exceeds " + what +
-                            human_bytes(budget) + " (reduce --seg-size or --gpus)");
     return est;
 }
 

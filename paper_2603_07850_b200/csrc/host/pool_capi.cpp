@@ -32,8 +32,9 @@ struct ShmHeader {
     uint64_t start, limit, span;
     std::atomic<uint64_t> cursor;
     std::atomic<uint32_t> attached; // processes on this cursor (the tail-limit hint)
+    std::atomic<uint32_t> stop;     // cooperative stop of every attached rank (pool.cpp:104-111)
 };
-constexpr uint64_t kMagic = 0x474f4c4442414348ull; // "GOLDBACH"
+constexpr uint64_t kMagic = 0x474f4c4442414332ull; // "GOLDBAC2" (layout with the stop word)
 
 int map_exception(const std::exception& e) {
     t_pool_err = e.what();
@@ -53,7 +54,7 @@ void to_c(const RunResult& r, gb_run_result* o) {
     o->max_p = r.min_prime.p;
     o->max_n = r.min_prime.n;
     o->segments = r.segments;
-    o->n_counterexamples = r.counterexamples.size();
+    o->n_counterexamples = std::max<uint64_t>(r.counterexample_count, r.counterexamples.size());
     for (size_t i = 0; i < r.counterexamples.size() && i < GB_REC_MAX_CE; ++i) o->counterexamples[i] = r.counterexamples[i];
     o->wall_seconds = r.wall_seconds;
 }
@@ -97,6 +98,7 @@ int gb_pool_create(uint64_t start, uint64_t limit, uint64_t seg_size, const char
                 p->shm->span = 2 * seg_size;
                 new (&p->shm->cursor) std::atomic<uint64_t>(start);
                 new (&p->shm->attached) std::atomic<uint32_t>(0);
+                new (&p->shm->stop) std::atomic<uint32_t>(0);
                 std::atomic_thread_fence(std::memory_order_release);
                 p->shm->magic = kMagic;
             } else if (p->shm->magic != kMagic || p->shm->start != start || p->shm->limit != limit ||
@@ -105,7 +107,8 @@ int gb_pool_create(uint64_t start, uint64_t limit, uint64_t seg_size, const char
                 throw ParamError("gb_pool_create: shared pool " + p->name + " does not match these bounds");
             }
             p->shm->attached.fetch_add(1, std::memory_order_relaxed);
-            p->pool = std::make_unique<WorkPool>(start, limit, seg_size, &p->shm->cursor, &p->shm->attached);
+            p->pool = std::make_unique<WorkPool>(start, limit, seg_size, &p->shm->cursor, &p->shm->attached,
+                                                 &p->shm->stop);
         }
         *out = p.release();
         return GB_OK;
@@ -123,6 +126,14 @@ int gb_pool_claim(gb_pool* p, uint64_t* a, uint64_t* b, uint64_t* index) {
     *index = j->index;
     return 1;
 }
+
+int gb_pool_request_stop(gb_pool* p) {
+    if (!p) return GB_ERR_PARAM;
+    p->pool->request_stop();
+    return GB_OK;
+}
+
+int gb_pool_stop_requested(const gb_pool* p) { return p && p->pool->stop_requested() ? 1 : 0; }
 
 int gb_pool_destroy(gb_pool* p, int unlink) {
     if (!p) return GB_OK;
@@ -167,7 +178,11 @@ int gb_drain_pool(gb_dev* dev, gb_pool* pool, int max_inflight, gb_run_result* o
         mine.min_prime.merge(MinPrimeMax{r.max_p, r.max_n});
         for (uint64_t i = 0; i < r.n_counterexamples && i < GB_REC_MAX_CE; ++i)
             mine.counterexamples.push_back(r.counterexamples[i]);
-        if (r.n_counterexamples) stop = true;
+        mine.counterexample_count += r.n_counterexamples;
+        if (r.n_counterexamples) {
+            stop = true;
+            pool->pool->request_stop(); // reaches every rank on a shared cursor
+        }
         depth = std::min(cap, depth * 2);
     }
     std::sort(mine.counterexamples.begin(), mine.counterexamples.end());

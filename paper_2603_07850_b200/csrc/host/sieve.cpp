@@ -104,7 +104,7 @@ OddBitset tiled_sieve_segment(uint64_t lo, uint64_t hi, const BasePrimes& base, 
     const uint64_t s = base.sqrt_bound;
     if (s == 0 || s < hi / s) throw ParamError("tiled_sieve_segment: base primes insufficient for segment bound");
     OddBitset out = OddBitset::new_filled(lo, hi);
-    auto sd = util_device(base.cover_limit ? base.cover_limit : s * s);
+    auto sd = util_device(cover_limit_of(base));
     sd->with([&](Device& d) {
         auto w = out.words();
         d.check(gb_sieve_interval(d.get(), lo, hi, w.data(), w.size()));

@@ -22,7 +22,7 @@ void check_job(const SegmentJob& job) {
 DeviceConfig config_of(const VerifyContext& ctx, uint64_t max_seg_evens) {
     DeviceConfig c;
     c.device = ctx.devices.empty() ? 0 : ctx.devices.front();
-    c.cover_limit = ctx.base->cover_limit ? ctx.base->cover_limit : ctx.base->sqrt_bound * ctx.base->sqrt_bound;
+    c.cover_limit = cover_limit_of(*ctx.base);
     c.p_small = ctx.small->p_small;
     c.inject_fail = ctx.inject_fail;
     c.max_seg_evens = max_seg_evens;

@@ -35,6 +35,13 @@ std::vector<uint64_t> simple_sieve(uint64_t limit, uint64_t mem_cap_bytes = uint
 // Minimal s with s >= cover_limit / s (sieve.cpp:48-52); pure integer math.
 uint64_t sqrt_bound_for(uint64_t cover_limit);
 
+// The limit a caller-built BasePrimes covers: its cover_limit, else
+// sqrt_bound^2 saturated at 2^64 - 1 (s = 2^32 covers every u64).
+inline uint64_t cover_limit_of(const BasePrimes& b) {
+    if (b.cover_limit) return b.cover_limit;
+    return b.sqrt_bound >= (uint64_t{1} << 32) ? ~uint64_t{0} : b.sqrt_bound * b.sqrt_bound;
+}
+
 // K1 on the device (sieve.hpp:34).
 BasePrimes build_base_primes(uint64_t cover_limit);
 

@@ -110,6 +110,15 @@ static void test_pool() {
         auto ja = a.claim_next(), jb = b.claim_next();
         CHECK(ja && jb && ja->a == 4 && jb->a == 24 && !a.claim_next() && !b.claim_next());
     }
+    {   // shared stop word: a stop requested through one pool ends claims on both
+        std::atomic<uint64_t> cur{4};
+        std::atomic<uint32_t> workers{2}, stop{0};
+        WorkPool a(4, 400, 10, &cur, &workers, &stop), b(4, 400, 10, &cur, &workers, &stop);
+        CHECK(a.claim_next() && b.claim_next() && !a.stop_requested());
+        a.request_stop();
+        CHECK(b.stop_requested() && !b.claim_next() && !a.claim_next());
+        CHECK(cur.load() == 44); // no claim advanced the cursor after the stop
+    }
     {
         std::ostringstream sink;
         Logger log(sink);
@@ -216,6 +225,15 @@ static void test_verifier_host() {
     // sqrt_bound (test_sieve.cpp:48-62)
     CHECK(sqrt_bound_for(1) == 1 && sqrt_bound_for(4) == 2 && sqrt_bound_for(11) == 3 && sqrt_bound_for(12) == 4);
     CHECK(sqrt_bound_for(~uint64_t{0} - 1) == (uint64_t{1} << 32));
+    // a caller-built BasePrimes without cover_limit: s^2 saturates at s = 2^32
+    BasePrimes top;
+    top.sqrt_bound = uint64_t{1} << 32;
+    CHECK(cover_limit_of(top) == ~uint64_t{0});
+    CHECK(sqrt_bound_for(cover_limit_of(top)) == top.sqrt_bound);
+    top.sqrt_bound = 1000;
+    CHECK(cover_limit_of(top) == 1'000'000);
+    top.cover_limit = 999'999;
+    CHECK(cover_limit_of(top) == 999'999);
 }
 
 // ---- cli (test_cli.cpp:24-155)

@@ -95,3 +95,47 @@ def test_merge_rules():
     assert m["sum_pmin"] == 1 and m["evens"] == 11 and (m["max_p"], m["max_n"]) == (7, 90)
     assert m["ce"] == [20, 50] and m["n_ce"] == 2
     assert gd.unpack(gd.pack(m)) == m
+
+
+def _stop_worker(rank, world, port, shm, q):
+    import sys
+    sys.path.insert(0, ROOT)
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    import paper_2603_07850_b200 as gb
+    start, limit, seg = 4, 2_000_002, 1000
+    pool = gb.Pool(start, limit, seg, shm_name=shm, create=True) if rank == 0 else None
+    dist.barrier()
+    if rank != 0:
+        pool = gb.Pool(start, limit, seg, shm_name=shm, create=False)
+    claimed = []
+    if rank == 1:
+        # rank 1 "finds a counterexample" in its second segment and stops
+        # the shared pool, as run_workers / gb_drain_pool do (pool.cpp:104-111)
+        claimed += [pool.claim(), pool.claim()]
+        pool.request_stop()
+    dist.barrier()
+    stopped = pool.stop_requested
+    while (j := pool.claim()) is not None:
+        claimed.append(j)
+    dist.barrier()
+    pool.close(unlink=(rank == 0))
+    q.put((rank, stopped, claimed))
+    dist.destroy_process_group()
+
+
+def test_stop_reaches_every_rank_on_a_shared_cursor():
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    shm = f"/gb_gloo_stop_{os.getpid()}_{port}"
+    procs = [ctx.Process(target=_stop_worker, args=(r, 2, port, shm, q)) for r in (0, 1)]
+    for p in procs:
+        p.start()
+    out = dict((r, (s, c)) for r, s, c in (q.get(timeout=120) for _ in procs))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    assert out[0][0] and out[1][0]                 # both ranks see the stop word
+    assert out[0][1] == []                         # rank 0 claims nothing after it
+    assert [j[2] for j in out[1][1]] == [0, 1]     # only the segments claimed before the stop

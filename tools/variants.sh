@@ -3,7 +3,7 @@
 #   tools/variants.sh NAME "GEN_ARGS" "EXTRA_NVFLAGS" [NAME "GEN_ARGS" "EXTRA_NVFLAGS" ...]
 # Each variant lands in build/variants/NAME/libgoldbach_b200.so; the in-tree
 # header and library are rebuilt with the defaults afterwards.
-# Time them with: GB_LIB_PATH=build/variants/NAME/libgoldbach_b200.so python tools/quick_bench.py 1e12
+# Time them with: GB_TOOLS_LIB_OVERRIDE=1 GB_LIB_PATH=build/variants/NAME/libgoldbach_b200.so python tools/quick_bench.py 1e12
 set -e
 cd "$(dirname "$0")/.."
 while [ $# -ge 3 ]; do
