@@ -2,6 +2,7 @@
 #   paper_2603_07850_b200/libgoldbach_b200.so   CUDA kernels + C-ABI + C++ host layer
 #   paper_2603_07850_b200/bin/goldbach           the CLI (drop-in for proj/tools/main.cpp)
 #   paper_2603_07850_b200/bin/test_host          C++ unit tests of the host layer
+#   paper_2603_07850_b200/bin/ref_api_conformance every reference API symbol, exact signatures
 #   oracle/liboracle.so                          CPU oracle (test infrastructure)
 NVCC ?= nvcc
 CXX ?= g++
@@ -37,7 +38,8 @@ $(LIB): $(CU_OBJS) $(HOST_OBJS)
 cli: $(LIB)
 	@if [ -f $(CSRC)/tools/goldbach_main.cpp ]; then mkdir -p $(BIN) && \
 	  $(CXX) $(CXXFLAGS) $(CSRC)/tools/goldbach_main.cpp -o $(BIN)/goldbach -L$(PKG) -lgoldbach_b200 -Wl,-rpath,'$$ORIGIN/..' && \
-	  $(CXX) $(CXXFLAGS) $(CSRC)/tools/test_host.cpp -o $(BIN)/test_host -L$(PKG) -lgoldbach_b200 -Wl,-rpath,'$$ORIGIN/..'; fi
+	  $(CXX) $(CXXFLAGS) $(CSRC)/tools/test_host.cpp -o $(BIN)/test_host -L$(PKG) -lgoldbach_b200 -Wl,-rpath,'$$ORIGIN/..' && \
+	  $(CXX) $(CXXFLAGS) $(CSRC)/tools/ref_api_conformance.cpp -o $(BIN)/ref_api_conformance -L$(PKG) -lgoldbach_b200 -Wl,-rpath,'$$ORIGIN/..'; fi
 
 oracle:
 	$(MAKE) -C oracle

@@ -250,6 +250,27 @@ def cpu_reference_sample(args, cores: int, target_s: float = 15.0):
             "seconds": secs}
 
 
+def cli_process_time(args):
+    """Wall time of one `bin/goldbach LIMIT --gpus=1 --json` process (the
+    reference's user-facing command, cli.cpp:298-334), measured twice; its
+    JSON summary must agree with the device-timed passes."""
+    exe = os.path.join(ROOT, "paper_2603_07850_b200", "bin", "goldbach")
+    if not os.path.exists(exe):
+        return None
+    walls, j = [], None
+    for _ in range(2):
+        t0 = time.perf_counter()
+        out = subprocess.run([exe, str(args.limit), "--gpus=1", "--json", f"--seg-size={args.seg_size}",
+                              f"--p-small={args.p_small}"], capture_output=True, text=True, timeout=900)
+        walls.append(time.perf_counter() - t0)
+        if out.returncode != 0:
+            return {"error": out.stderr[-300:]}
+        j = json.loads(out.stdout.strip().splitlines()[-1])
+    return {"process_s": min(walls), "runs_s": walls, "wall_seconds_reported": j.get("wall_seconds"),
+            "max_min_prime": j.get("max_min_prime"), "max_min_prime_n": j.get("max_min_prime_n"),
+            "total_evens": j.get("total_evens")}
+
+
 def host_cores() -> int:
     try:
         return len(os.sched_getaffinity(0))
@@ -307,6 +328,7 @@ def main():
     ap.add_argument("--seg-size", type=int, default=SPAN_DEFAULT)
     ap.add_argument("--p-small", type=int, default=1_000_000)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-cli", action="store_true", help="skip the CLI process timing")
     ap.add_argument("--ref-warmup", action="store_true",
                     help="also run the warm-up steps in the reference arm")
     args = ap.parse_args()
@@ -326,8 +348,12 @@ def main():
 
     import paper_2603_07850_b200 as gb
 
+    # cold open: the first handle of this process (CUDA context, module,
+    # K1 base primes, batch buffers) -- the init cost a CLI run pays
+    t_open = time.perf_counter()
     dev = gb.Device(args.limit, p_small=args.p_small, device=D.gpu,
                     max_seg_evens=args.seg_size)
+    cold_open_s = D.max(time.perf_counter() - t_open)
     total_evens = (args.limit - args.start) // 2 + 1
 
     def pass_once(name, timed):
@@ -421,6 +447,16 @@ def main():
             e2e_s.append(dt)
     e2e_value = args.steps * total_evens / sum(e2e_s)
 
+    # warm open (context up, arena reused): what a second handle costs
+    t_open = time.perf_counter()
+    gb.Device(args.limit, p_small=args.p_small, device=D.gpu, max_seg_evens=args.seg_size).close()
+    warm_open_s = D.max(time.perf_counter() - t_open)
+    # the whole CLI process (bin/goldbach LIMIT --gpus=1 --json): cold
+    # process start, context, tables, drain, summary -- the user's wall time
+    cli = None
+    if D.world == 1 and args.start == 4 and not args.no_cli:
+        cli = cli_process_time(args)
+
     cpu = None
     if D.world == 1 and not args.no_cpu_baseline:
         cpu = cpu_reference_sample(args, host_cores())
@@ -444,6 +480,10 @@ def main():
             "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": h2d,
                     "d2h_bytes_per_step": d2h, "seconds_per_step": sum(e2e_s) / args.steps,
                     "step_seconds": e2e_s},
+            "init": {"cold_open_s": cold_open_s, "warm_open_s": warm_open_s,
+                     "note": "gb_open on the bench GPU: first handle of the process (CUDA "
+                             "context, module, device K1 tables, buffers) and a second one"},
+            "cli_process_s": cli,
             "gpu_launches": launches,
             "roofline": roofline,
             "cpu_baseline": ({k: cpu[k] for k in ("value", "unit", "cores", "kind", "sample")}

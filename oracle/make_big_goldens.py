@@ -101,14 +101,18 @@ def load(path: str):
     return done
 
 
-def run_set(name: str, jobs: int, stride: int = 1):
+def run_set(name: str, jobs: int, stride: int = 1, part=None, out=None, skip=None):
     cfg = SETS[name]
     segs = segments(cfg["start"], cfg["limit"])
     os.makedirs(BIG, exist_ok=True)
-    path = os.path.join(BIG, f"{name}.tsv")
+    path = out or os.path.join(BIG, f"{name}.tsv")
     done = load(path)
+    if skip:  # records already produced elsewhere (e.g. on another host)
+        for p in skip:
+            done.update(load(p))
+    lo, hi = part if part else (0, len(segs))
     todo = [segs[i] for i in stride_order(len(segs))
-            if segs[i][0] not in done and (i % stride == 0 or i == len(segs) - 1)]
+            if lo <= i < hi and segs[i][0] not in done and (i % stride == 0 or i == len(segs) - 1)]
     print(f"{name}: {len(segs)} segments, {len(done)} done, {len(todo)} to go", flush=True)
     t0 = time.time()
     with ProcessPoolExecutor(jobs) as ex, open(path, "a") as f:
@@ -175,6 +179,10 @@ def main():
     ap.add_argument("--set", choices=sorted(SETS))
     ap.add_argument("--jobs", type=int, default=max(1, (os.cpu_count() or 2) - 1))
     ap.add_argument("--stride", type=int, default=1, help="only every k-th segment (+ the last)")
+    ap.add_argument("--part", help="only segment indices i0:i1")
+    ap.add_argument("--out", help="records file (default oracle/_big/<set>.tsv)")
+    ap.add_argument("--skip", action="append", help="records files whose segments are done")
+    ap.add_argument("--merge", action="append", help="records files to merge into oracle/_big/<set>.tsv")
     ap.add_argument("--pack", action="store_true")
     ap.add_argument("--selfcheck", action="store_true")
     a = ap.parse_args()
@@ -182,8 +190,19 @@ def main():
         sys.exit("oracle/_ref/libref.so missing: run oracle/build_ref.sh first")
     if a.selfcheck:
         selfcheck()
-    if a.set:
-        run_set(a.set, a.jobs, a.stride)
+    if a.set and a.merge:
+        path = os.path.join(BIG, f"{a.set}.tsv")
+        done = load(path)
+        n0 = len(done)
+        for p in a.merge:
+            done.update(load(p))
+        with open(path, "w") as f:
+            for idx in sorted(done):
+                f.write(" ".join(str(x) for x in done[idx]) + "\n")
+        print(f"merged: {n0} -> {len(done)} records")
+    elif a.set:
+        part = tuple(int(x) for x in a.part.split(":")) if a.part else None
+        run_set(a.set, a.jobs, a.stride, part, a.out, a.skip)
     if a.pack:
         pack()
 

@@ -149,6 +149,8 @@ def lib():
         "gb_launch_count": ([vp, p64], i32),
         "gb_kernel_times": ([vp, C.POINTER(C.c_double), p64, i32], i32),
         "gb_set_timing": ([vp, i32], i32),
+        "gb_set_bucket": ([vp, i32], i32),
+        "gb_bucket_info": ([vp, p64], i32),
         "gb_io_bytes": ([vp, p64, p64], i32),
         "gb_flush_l2": ([vp], i32),
         "gb_synchronize": ([vp], i32),
@@ -319,6 +321,16 @@ class Device:
     def set_timing(self, mode):
         """0/False off, 1/True event timing, 2 timing with serialised batches."""
         _check(lib().gb_set_timing(self._h, int(mode)), self._h)
+
+    def set_bucket(self, enabled: bool):
+        """Bucket sieve of the large primes on/off (results are identical)."""
+        _check(lib().gb_set_bucket(self._h, 1 if enabled else 0), self._h)
+
+    def bucket_info(self) -> dict:
+        v = (C.c_uint64 * 8)()
+        _check(lib().gb_bucket_info(self._h, v), self._h)
+        keys = ("active", "p0", "primes", "chunks", "cap", "blocks", "expect", "fallbacks")
+        return dict(zip(keys, list(v)))
 
     def io_bytes(self):
         h, d = C.c_uint64(), C.c_uint64()

@@ -464,13 +464,6 @@ __global__ void __launch_bounds__(256) k_large_strike(const SegJob* __restrict__
     }
 }
 
-// ============================================================ K2 + K3
-// Wheel-6 tile: [TPAD][A: M6W words][TPAD][B: M6W words][TPAD], pads zero.
-__device__ __forceinline__ uint32_t* arr_a(uint32_t* t) { return t + TPAD; }
-__device__ __forceinline__ uint32_t* arr_b(uint32_t* t) { return t + 2 * TPAD + M6W; }
-__device__ __forceinline__ const uint32_t* arr_a(const uint32_t* t) { return t + TPAD; }
-__device__ __forceinline__ const uint32_t* arr_b(const uint32_t* t) { return t + 2 * TPAD + M6W; }
-
 // Window cells of the first strikes of {p, m, z, c'} in arrays A and B of
 // the block starting at cell KB: z = k0 + p ceil(2^29 / p) (so z - KB >= 0
 // for every block start), A's offset is (z - KB) mod p by the magic
@@ -485,6 +478,163 @@ __device__ __forceinline__ void block_off6(const uint4 v, uint32_t KB, uint32_t&
     const uint32_t t = oa + v.w;
     ob = min(t, t - p);
 }
+
+// ============================================================ bucket fill
+// Lanes with the same block bin file their hits with one shared atomic per
+// bin (warp-collective: every lane calls it; act = the lane has a hit).  A
+// bin whose staging is full spills the hit straight to the global list.
+struct BkStage {
+    uint32_t* stage;  // [rb][capl]
+    uint32_t* cnt;    // [rb]
+    uint32_t capl;
+    uint32_t* gl;     // global list of bin 0 of the range ([bin][cap])
+    uint32_t* gc;     // global counts of bin 0 of the range
+    uint64_t cap;
+    unsigned int* flag;
+};
+
+__device__ __forceinline__ void bk_emit(const BkStage& S, bool act, uint32_t bin, uint32_t u, uint32_t lane) {
+    const uint32_t peers = __match_any_sync(0xffffffffu, act ? bin : 0xFFFFFFFFu);
+    if (!act) return;
+    const uint32_t leader = __ffs(peers) - 1;
+    uint32_t base = 0;
+    if (lane == leader) base = atomicAdd(&S.cnt[bin], (uint32_t)__popc(peers));
+    base = __shfl_sync(peers, base, leader) + __popc(peers & ((1u << lane) - 1));
+    if (base < S.capl) {
+        S.stage[bin * S.capl + base] = u;
+    } else {
+        const uint32_t g = atomicAdd(&S.gc[bin], 1u);
+        if (g < S.cap) S.gl[(size_t)bin * S.cap + g] = u;
+        else atomicOr(S.flag, 1u);
+    }
+}
+
+// Hits of one class array in blocks [B0, B1) of the piece: o is the prime's
+// first multiple at or after cell E0 = B0 K6 (relative to the slot origin).
+// Every multiple below E1 = B1 K6 is filed under its block, and under the
+// block before when it lies in the windows' overlap; the first multiple at
+// or after E1 files only its overlap copy (block B1 - 1), since its own
+// block belongs to the next range.  On return o is the first multiple
+// >= E1 (0xFFFFFFFF once past 2^32).  Warp-collective.
+__device__ __forceinline__ void bk_run(const BkStage& S, uint32_t& o, uint32_t p, bool has, uint32_t enc,
+                                       uint32_t B0, uint32_t E1, uint32_t nbins, uint32_t lane) {
+    for (;;) {
+        const bool act = has && o < E1;
+        if (!__any_sync(0xffffffffu, act)) break;
+        const uint32_t b = o / K6; // constant divisor: multiply-high
+        const uint32_t w = o - b * K6;
+        bk_emit(S, act, b - B0, enc + w, lane);
+        const bool dup = act && w < DUP6 && b > B0;
+        if (__any_sync(0xffffffffu, dup)) bk_emit(S, dup, b - 1 - B0, enc + w + K6, lane);
+        if (act) o = p >= 0xFFFFFFFFu - o ? 0xFFFFFFFFu : o + p;
+    }
+    const bool tail = has && o != 0xFFFFFFFFu && o - E1 < DUP6;
+    if (__any_sync(0xffffffffu, tail)) bk_emit(S, tail, nbins - 1, enc + (o - E1) + K6, lane);
+}
+
+// first multiple >= E0 of a progression k0 + j p (k0 < p), 32-bit; m32 <=
+// floor(2^32 / p) makes the quotient estimate low by at most 2
+__device__ __forceinline__ uint32_t first_ge(uint32_t k0, uint32_t E0, uint32_t p, uint32_t m32) {
+    if (k0 >= E0) return k0;
+    const uint32_t x = E0 - k0;       // < 2^29
+    uint32_t q = __umulhi(x, m32);
+    uint32_t r = x - q * p;
+    while (r >= p) { r -= p; ++q; }
+    const uint64_t o = (uint64_t)k0 + (uint64_t)(q + (r != 0)) * p;
+    return o > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)o;
+}
+
+// One CTA per (chunk, slot): blockIdx.x = chunk * nslots + slot, so the
+// slots of one chunk run side by side and share its primes in L2.
+__global__ void __launch_bounds__(BK_THREADS, 2) k_bucket_fill(BucketArgs A) {
+    extern __shared__ __align__(16) uint32_t bsm[];
+    const uint32_t s = blockIdx.x % A.nslots;
+    const BktChunk C = A.chunks[blockIdx.x / A.nslots];
+    const SegJob J = A.jobs[s];
+    const uint32_t nb = J.nblocks;
+    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    constexpr uint32_t NW = BK_THREADS / 32;
+    BkStage S;
+    S.stage = bsm;
+    S.cnt = bsm + C.rb * C.capl;
+    S.capl = C.capl;
+    S.cap = A.bk_cap;
+    S.flag = A.flag;
+    for (uint32_t i = threadIdx.x; i < C.rb; i += BK_THREADS) S.cnt[i] = 0;
+    const bool dense = C.i1 <= A.iA0 + A.np;
+    // dense chunk: one prime per thread, carried across the ranges
+    uint32_t p = 0, oA = 0xFFFFFFFFu, oB = 0xFFFFFFFFu;
+    bool has = false;
+    if (dense) {
+        const uint32_t i = C.i0 + threadIdx.x;
+        has = i < C.i1;
+        if (has) {
+            const uint4 v = A.pmc[(size_t)s * A.np + (i - A.iA0)];
+            p = v.x;
+            block_off6(v, 0, oA, oB);
+        }
+    }
+    __syncthreads();
+    for (uint32_t B0 = 0; B0 < nb; B0 += C.rb) {
+        const uint32_t B1 = min(nb, B0 + C.rb);
+        const uint32_t E0 = B0 * K6, E1 = B1 * K6;
+        const size_t key0 = (size_t)s * A.bk_nb + B0;
+        S.gl = A.bkt + key0 * A.bk_cap;
+        S.gc = A.bcnt + key0;
+        if (dense) {
+            bk_run(S, oA, p, has, BK_ENC_A, B0, E1, B1 - B0, lane);
+            bk_run(S, oB, p, has, BK_ENC_B, B0, E1, B1 - B0, lane);
+        } else {
+            // sparse: many primes per thread, first multiples from scratch
+            for (uint32_t ib = C.i0 + warp * 32; ib < C.i1; ib += BK_THREADS) {
+                const uint32_t i = ib + lane;
+                const bool h = i < C.i1;
+                uint32_t q = 0, a = 0xFFFFFFFFu, bb = 0xFFFFFFFFu;
+                if (h) {
+                    q = A.primes[i];
+                    const uint64_t m = A.m64[i];
+                    const uint32_t k0 = first_a6(J, q, m);
+                    const uint32_t c = b_shift6(q);
+                    const uint32_t k0b = k0 >= c ? k0 - c : k0 + (q - c);
+                    const uint32_t m32 = (uint32_t)(m >> 32);
+                    a = first_ge(k0, E0, q, m32);
+                    bb = first_ge(k0b, E0, q, m32);
+                }
+                bk_run(S, a, q, h, BK_ENC_A, B0, E1, B1 - B0, lane);
+                bk_run(S, bb, q, h, BK_ENC_B, B0, E1, B1 - B0, lane);
+            }
+        }
+        __syncthreads();
+        // flush: one global reservation per bin, coalesced copy
+        for (uint32_t bin = warp; bin < B1 - B0; bin += NW) {
+            const uint32_t n = min(S.cnt[bin], C.capl);
+            __syncwarp();
+            if (n) {
+                uint64_t base = 0;
+                if (lane == 0) {
+                    base = atomicAdd(&S.gc[bin], n);
+                    S.cnt[bin] = 0;
+                    if (base + n > A.bk_cap) atomicOr(A.flag, 1u);
+                }
+                base = __shfl_sync(0xffffffffu, base, 0);
+                uint32_t* dst = S.gl + (size_t)bin * A.bk_cap;
+                const uint32_t* src = S.stage + bin * C.capl;
+                for (uint32_t j = lane; j < n; j += 32)
+                    if (base + j < A.bk_cap) dst[base + j] = src[j];
+            } else if (lane == 0) {
+                S.cnt[bin] = 0;
+            }
+        }
+        __syncthreads();
+    }
+}
+
+// ============================================================ K2 + K3
+// Wheel-6 tile: [TPAD][A: M6W words][TPAD][B: M6W words][TPAD], pads zero.
+__device__ __forceinline__ uint32_t* arr_a(uint32_t* t) { return t + TPAD; }
+__device__ __forceinline__ uint32_t* arr_b(uint32_t* t) { return t + 2 * TPAD + M6W; }
+__device__ __forceinline__ const uint32_t* arr_a(const uint32_t* t) { return t + TPAD; }
+__device__ __forceinline__ const uint32_t* arr_b(const uint32_t* t) { return t + 2 * TPAD + M6W; }
 
 // Warp-cooperative strikes of one prime in one class array from cell o:
 // lane L strikes o + L p + k 32p; 32p cells are p words, so the lane's mask
@@ -579,7 +729,8 @@ __device__ __forceinline__ void strike_rows(uint32_t* A6, uint32_t* B6, const ui
 // strike each array at most once.  pmc: this slot's rows (index i - iA0).
 template <int GT>
 __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __restrict__ pmc, uint32_t nA,
-                                               uint32_t nQ, uint32_t nH, uint32_t nW, uint32_t nB, uint32_t KB,
+                                               uint32_t nQ, uint32_t nH, uint32_t nW, uint32_t nB, uint32_t nK,
+                                               uint32_t KB,
                                                uint32_t tid,
                                                const uint16_t* __restrict__ wsplit) {
     const uint32_t lane = tid & 31, warp = tid >> 5;
@@ -605,6 +756,11 @@ __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __re
     // thread per prime; the rows come from L2, so several are loaded before
     // their strikes to keep loads in flight per warp.  Primes >= M6/4 strike
     // an array at most 4 (>= M6/2: 2, >= M6: 1) times, unrolled branch-free.
+    // rows end at nK (the first bucket prime; nB when the bucket sieve is off)
+    nQ = min(nQ, nK);
+    nH = min(nH, nK);
+    nW = min(nW, nK);
+    nB = min(nB, nK);
     strike_rows<GT, 0, GB_RUN_INFLIGHT>(A6, B6, pmc + nA + tid, pmc + nQ, KB, lane);
     strike_rows<GT, 4, GB_RUN_INFLIGHT>(A6, B6, pmc + nQ + tid, pmc + nH, KB, lane);
     constexpr int SS_INFLIGHT = GT == 32 * WS_SW_LIGHT ? GB_SS_INFLIGHT_LIGHT : GB_SS_INFLIGHT_HEAVY;
@@ -612,6 +768,49 @@ __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __re
 #ifndef GB_SKIP_SINGLE // timing probe: no single-strike primes (wrong results)
     strike_rows<GT, 1, SS_INFLIGHT>(A6, B6, pmc + nW + tid, pmc + nB, KB, lane);
 #endif
+}
+
+#ifndef GB_BK_INFLIGHT
+#define GB_BK_INFLIGHT 4 // 16-B hit loads in flight per thread
+#endif
+// one bucket hit: RED.AND of bit u & 31 of tile word u >> 5 (tb: the tile's
+// shared address)
+__device__ __forceinline__ void strike_cell(uint32_t tb, uint32_t u) {
+    asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(tb + ((u >> 3) & ~3u)),
+                 "r"(__funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, u))
+                 : "memory");
+}
+
+// Bucket hits of one block (k_bucket_fill's list) by a group of GT threads:
+// 16-B loads, GB_BK_INFLIGHT per thread in flight, then their REDs.
+template <int GT>
+__device__ __forceinline__ void strike_bucket(uint32_t* tile, const uint32_t* __restrict__ e, uint32_t n,
+                                              uint32_t tid) {
+    const uint32_t tb = (uint32_t)__cvta_generic_to_shared(tile);
+    const uint4* e4 = reinterpret_cast<const uint4*>(e);
+    const uint32_t n4 = n >> 2; // full quads
+    constexpr int U = GB_BK_INFLIGHT;
+    uint32_t i = tid;
+    for (; i + (U - 1) * GT < n4; i += U * GT) {
+        uint4 v[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) v[u] = __ldcs(e4 + i + u * GT);
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            strike_cell(tb, v[u].x);
+            strike_cell(tb, v[u].y);
+            strike_cell(tb, v[u].z);
+            strike_cell(tb, v[u].w);
+        }
+    }
+    for (; i < n4; i += GT) {
+        const uint4 v = __ldcs(e4 + i);
+        strike_cell(tb, v.x);
+        strike_cell(tb, v.y);
+        strike_cell(tb, v.z);
+        strike_cell(tb, v.w);
+    }
+    if (tid < (n & 3)) strike_cell(tb, __ldcs(e + 4 * n4 + tid));
 }
 
 // Presieve one class array (M6W words) with the wheel-6 patterns; ph[g] =
@@ -1183,8 +1382,13 @@ __device__ __forceinline__ void sieve_block(const VerifyArgs& A, uint32_t* tile,
     gbar<GT>(bar);
 #ifndef GB_SKIP_STRIKES // timing probe: the check group on presieved-only tiles
     strike_verify6<GT>(tile, A.pmc + (size_t)I.s * A.np, A.iA1 - A.iA0, A.iQ1 - A.iA0, A.iH1 - A.iA0,
-                       A.iW1 - A.iA0, A.iB1 - A.iA0, I.KB, tid,
+                       A.iW1 - A.iA0, A.iB1 - A.iA0, A.iK0 - A.iA0, I.KB, tid,
                        A.wsplit);
+    if (A.bk_cnt != nullptr) {
+        const size_t key = (size_t)I.s * A.bk_nb + I.b;
+        const uint32_t n = (uint32_t)min((uint64_t)A.bk_cnt[key], A.bk_cap);
+        strike_bucket<GT>(tile, A.bkt + key * A.bk_cap, n, tid);
+    }
 #endif
     if (A.qg != nullptr && I.J.qg_words) {
         gbar<GT>(bar);
@@ -1509,7 +1713,8 @@ __device__ void add_ce(DevRecord& r, uint64_t n) {
 
 __global__ void k_finalize(const SegJob* __restrict__ jobs, uint32_t nslots, const SlotAcc* __restrict__ acc,
                            const StragEntry* __restrict__ list, const unsigned int* __restrict__ list_count,
-                           uint32_t list_cap, const StragResult* __restrict__ res, DevRecord* __restrict__ out) {
+                           uint32_t list_cap, const StragResult* __restrict__ res,
+                           const unsigned int* __restrict__ bk_flag, DevRecord* __restrict__ out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     uint32_t cnt = *list_count;
     for (uint32_t s = 0; s < nslots; ++s) {
@@ -1525,7 +1730,7 @@ __global__ void k_finalize(const SegJob* __restrict__ jobs, uint32_t nslots, con
             r.max_p = k >> 32;
             r.max_n = J.a + 2ull * (0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFu));
         }
-        r.overflow = cnt > list_cap;
+        r.overflow = (cnt > list_cap ? 1u : 0u) | (bk_flag && *bk_flag ? 2u : 0u);
         out[s] = r;
     }
     uint32_t m = min(cnt, list_cap);
@@ -1663,6 +1868,11 @@ cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint3
                                                                                  iL1, qg, qg_stride_words);
     return cudaGetLastError();
 }
+cudaError_t launch_bucket_fill(const BucketArgs& a, uint32_t nchunks, cudaStream_t st) {
+    if (!nchunks || !a.nslots) return cudaSuccess;
+    k_bucket_fill<<<nchunks * a.nslots, BK_THREADS, BK_STAGE_WORDS * 4, st>>>(a);
+    return cudaGetLastError();
+}
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st) {
     if (a.nslots > MAX_SLOTS) return cudaErrorInvalidValue; // s_jobs holds MAX_SLOTS
     // the sieve/check split follows the sieve's share of the work, which
@@ -1684,8 +1894,8 @@ cudaError_t launch_stragglers(const SegJob* jobs, const StragEntry* list, const 
 }
 cudaError_t launch_finalize(const SegJob* jobs, uint32_t nslots, const SlotAcc* acc, const StragEntry* list,
                             const unsigned int* list_count, uint32_t list_cap, const StragResult* res,
-                            DevRecord* out, cudaStream_t st) {
-    k_finalize<<<1, 32, 0, st>>>(jobs, nslots, acc, list, list_count, list_cap, res, out);
+                            const unsigned int* bk_flag, DevRecord* out, cudaStream_t st) {
+    k_finalize<<<1, 32, 0, st>>>(jobs, nslots, acc, list, list_count, list_cap, res, bk_flag, out);
     return cudaGetLastError();
 }
 cudaError_t launch_phase2_one(uint64_t n, uint64_t* out, cudaStream_t st) {
@@ -1701,6 +1911,9 @@ cudaError_t launch_is_prime_batch(const uint64_t* v, uint8_t* out, uint64_t n, c
 int verify_occupancy(int* blocks_per_sm) {
     // per-device function attributes: call after cudaSetDevice
     if (cudaFuncSetAttribute(k_sieve_interval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SIEVE_SMEM) !=
+        cudaSuccess)
+        return 1;
+    if (cudaFuncSetAttribute(k_bucket_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(BK_STAGE_WORDS * 4)) !=
         cudaSuccess)
         return 1;
     if (cudaFuncSetAttribute(k_verify_ws<false, WS_SW_LIGHT>, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -24,4 +24,15 @@ std::vector<bool> is_prime_batch(const std::vector<uint64_t>& values) {
 
 bool is_prime_u64(uint64_t n) { return is_prime_batch({n})[0]; }
 
+uint64_t modpow(uint64_t a, uint64_t e, uint64_t m) {
+    if (m == 0) throw ParamError("modpow: modulus must be nonzero");
+    uint64_t r = 1 % m;
+    a %= m;
+    for (; e; e >>= 1) {
+        if (e & 1) r = modmul(r, a, m);
+        a = modmul(a, a, m);
+    }
+    return r;
+}
+
 } // namespace goldbach

@@ -3,6 +3,7 @@
 #include "goldbach/verifier.hpp"
 
 #include <algorithm>
+#include <bit>
 
 #include "goldbach/device.hpp"
 #include "goldbach/errors.hpp"
@@ -95,6 +96,52 @@ std::vector<uint64_t> phase1_min_primes(const SegmentJob& job, uint64_t p_small,
         d.check(gb_phase1_pmin(d.get(), job.a, job.b, out.data(), out.size()));
         return 0;
     });
+    return out;
+}
+
+Phase1Result phase1_verify(const SegmentJob& job, const SmallPrimeTable& small, const OddBitset& qbits,
+                           uint64_t batch_size, std::vector<uint64_t>* min_primes_out) {
+    check_job(job);
+    if (batch_size == 0) throw ParamError("phase1_verify: batch_size must be >= 1");
+    if (small.primes.empty() || small.primes.front() != 2)
+        throw ParamError("phase1_verify: malformed small-prime table");
+    const OddRange need = sieve_range_for(job, small.p_small);
+    if (qbits.lo() > need.lo || qbits.hi() < need.hi)
+        throw InternalError("phase1_verify: sieved range does not cover the q lookups");
+    const uint64_t n = ((job.b - job.a) >> 1) + 1;
+    Phase1Result res{PackedBits(n, false), {}};
+    if (min_primes_out) min_primes_out->assign(n, 0);
+    // device pieces of at most 2^20 - 16 evens (gb_phase1_pmin's limit)
+    const uint64_t piece = (uint64_t{1} << 20) - 16;
+    std::vector<uint64_t> part;
+    for (uint64_t i0 = 0; i0 < n; i0 += piece) {
+        const uint64_t m = std::min(piece, n - i0);
+        const SegmentJob sub{job.a + 2 * i0, job.a + 2 * (i0 + m - 1), job.index};
+        part = phase1_min_primes(sub, small.p_small, std::max<uint64_t>(job.b, 4));
+        for (uint64_t k = 0; k < m; ++k) {
+            const uint64_t p = part[k];
+            if (!p) continue;
+            res.verified.set(i0 + k);
+            res.min_prime.observe(p, sub.a + 2 * k);
+            if (min_primes_out) (*min_primes_out)[i0 + k] = p;
+        }
+    }
+    return res;
+}
+
+UnverifiedSet count_unverified(const PackedBits& verified, uint64_t a) {
+    if (a & 1) throw ParamError("count_unverified: a must be even");
+    const uint64_t zeros = verified.size() - verified.popcount();
+    if (zeros > UINT32_MAX) throw InternalError("count_unverified: count does not fit 32 bits");
+    UnverifiedSet out;
+    out.count = (uint32_t)zeros;
+    out.values.reserve(zeros);
+    const auto w = verified.words();
+    for (size_t k = 0; k < w.size(); ++k) {
+        uint64_t z = ~w[k];
+        if (k + 1 == w.size() && (verified.size() & 63)) z &= (uint64_t{1} << (verified.size() & 63)) - 1;
+        for (; z; z &= z - 1) out.values.push_back(a + 2 * ((uint64_t{k} << 6) + (uint64_t)std::countr_zero(z)));
+    }
     return out;
 }
 

@@ -106,3 +106,16 @@ def test_cpp_host_unit_tests():
     out = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert out.returncode == 0, out.stderr[-2000:]
     assert " 0 failed" in out.stdout
+
+
+def test_reference_api_conformance_host():
+    """Every symbol of the reference headers (proj/include/goldbach/*.hpp)
+    with its exact signature compiles and links against this library
+    (ref_api_conformance.cpp: static_asserts on pointer and member types);
+    the host-only entry points return the reference tests' known answers."""
+    exe = os.path.join(ROOT, "paper_2603_07850_b200", "bin", "ref_api_conformance")
+    if not os.path.exists(exe):
+        subprocess.run(["make", "-C", ROOT, "cli"], check=True, capture_output=True)
+    out = subprocess.run([exe], capture_output=True, text=True, timeout=120)
+    assert out.returncode == 0, out.stdout + out.stderr[-2000:]
+    assert "conformance ok" in out.stdout

@@ -93,3 +93,40 @@ def test_split_runs_sum():
                    .strip().splitlines()[-1])
     assert a["total_evens"] + b["total_evens"] == whole["total_evens"]
     assert max(a["max_min_prime"], b["max_min_prime"]) == whole["max_min_prime"]
+    # the checksums are sums over evens, the segments a partition of the range
+    M = (1 << 64) - 1
+    assert (a["pmin_sum"] + b["pmin_sum"]) & M == whole["pmin_sum"]
+    assert (a["pmin_hash"] + b["pmin_hash"]) & M == whole["pmin_hash"]
+    assert a["segments"] + b["segments"] == whole["segments"] + 1  # 2e9 / 4e8: the cut splits one segment
+    assert a["unverified_total"] + b["unverified_total"] == whole["unverified_total"] == 0
+    w = max((a, b), key=lambda r: (r["max_min_prime"], -r["max_min_prime_n"]))
+    assert w["max_min_prime_n"] == whole["max_min_prime_n"]
+
+
+@pytest.mark.gpu
+@need_bins
+@pytest.mark.parametrize("k", [1, 2, 4])
+def test_cli_worker_count_invariance(k):
+    """acceptance c6 (acceptance.cpp:188-248): --gpus=k workers (round-robin
+    over the visible GPUs, so k workers share GPU 0 on a 1-GPU box) give the
+    same totals, checksums and max for every k; every worker claims work."""
+    ro, out, err = run(OURS, "20000000000", "--json", f"--gpus={k}")
+    assert ro == 0, err
+    j = json.loads(out.strip().splitlines()[-1])
+    assert j["workers_used"] == k and len(j["per_worker_segments"]) == k
+    assert sum(j["per_worker_segments"]) == j["segments"] == 50
+    assert j["total_evens"] == 9_999_999_999 and j["unverified_total"] == 0
+    ref = json.loads(run(OURS, "20000000000", "--json", "--gpus=1")[1].strip().splitlines()[-1])
+    for key in ("total_evens", "pmin_sum", "pmin_hash", "max_min_prime", "max_min_prime_n", "segments"):
+        assert j[key] == ref[key], (key, j[key], ref[key])
+
+
+@pytest.mark.gpu
+@need_bins
+def test_cli_mem_cap_rejects_before_any_claim():
+    """validate_resources (cli.cpp:264-296): a cap below the per-GPU
+    footprint fails with exit 1 and a ResourceError before any work."""
+    ro, out, err = run(OURS, "10000000000000", "--mem-cap=1000000", "--json")
+    assert ro == 1
+    assert "mem" in err.lower() or "memory" in err.lower() or "exceeds" in err.lower(), err
+    assert out.strip() == ""

@@ -1,0 +1,120 @@
+"""Bucket sieve of the large base primes (k_bucket_fill + the fused kernel's
+list strikes) against the per-block row path and the reference goldens.
+
+The bucket sieve changes only WHERE a large prime's strikes come from (a
+per-block hit list filed once per piece instead of a row visited by every
+block), so every record must be bit-identical to the row path and to the
+reference (sieve.cpp:109-126, 144-147 is the reference's own hit list)."""
+import os
+
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+
+def _rec(dev, a, b):
+    return dev.verify_segment(a, b).key()
+
+
+def _open(gb, cover, **kw):
+    return gb.Device(cover, **kw)
+
+
+# (cover, segment a, segment evens): 1e12 / 1e13 (dense buckets, rows for the
+# first multiples), C5 height and the 2^64 ceiling (sparse buckets)
+CASES = [
+    (10**12, 10**12 - 400_000_000 + 2, 200_000_000),
+    (10**13, 9_000_000_000_004, 200_000_000),
+    (4 * 10**18 + 10**11, 4 * 10**18 + 4 * 10**9, 20_000_000),
+]
+
+
+@pytest.mark.parametrize("cover,a,n", CASES)
+def test_bucket_equals_rows(gpu, cover, a, n):
+    b = a + 2 * (n - 1)
+    with _open(gpu, cover) as dev:
+        info = dev.bucket_info()
+        assert info["active"] == 1 and info["primes"] > 0, info
+        got = _rec(dev, a, b)
+        dev.set_bucket(False)
+        want = _rec(dev, a, b)
+        dev.set_bucket(True)
+        assert dev.bucket_info()["fallbacks"] == 0
+    assert got == want
+
+
+def test_bucket_c2_records(gpu):
+    """All 25 C2 segments (reference records) with the threshold lowered to
+    2^16 so the bucket primes start inside C2's base primes (s = 1e5)."""
+    os.environ["GB_BKT_P"] = "65536"
+    try:
+        recs = golden("c2_segments.json")["records"]
+        with gpu.Device(10**10) as dev:
+            assert dev.bucket_info()["p0"] == 65537
+            for r in recs:
+                got = dev.verify_segment(r["a"], r["b"]).as_dict()
+                for k in ("evens", "unverified", "sum_pmin", "pos_hash", "max_p", "max_n"):
+                    assert got[k] == r[k], (k, r["a"], got, r)
+    finally:
+        del os.environ["GB_BKT_P"]
+
+
+@pytest.mark.parametrize("pb", ["65536", "131072", "524288", "1048576", "0"])
+def test_bucket_thresholds_agree(gpu, pb):
+    a, b = 10**13 - 40_000_000, 10**13
+    with gpu.Device(10**13) as dev:
+        want = _rec(dev, a, b)
+    os.environ["GB_BKT_P"] = pb
+    try:
+        with gpu.Device(10**13) as dev:
+            info = dev.bucket_info()
+            assert info["active"] == (0 if pb == "0" else 1)
+            assert _rec(dev, a, b) == want
+    finally:
+        del os.environ["GB_BKT_P"]
+
+
+def test_bucket_overflow_falls_back_to_rows(gpu):
+    """Lists far too small: every block overflows, the fill raises the flag
+    and the host re-runs the piece on the row path; results stay exact."""
+    a, b = 10**12 - 40_000_000, 10**12
+    with gpu.Device(10**12) as dev:
+        want = _rec(dev, a, b)
+    os.environ["GB_BKT_CAP_SCALE"] = "0.001"
+    try:
+        with gpu.Device(10**12) as dev:
+            got = _rec(dev, a, b)
+            assert dev.bucket_info()["fallbacks"] >= 1
+            # the asynchronous path too
+            dev.submit(a, b, 7)
+            r, tag = dev.wait()
+            assert tag == 7 and r.key() == want
+    finally:
+        del os.environ["GB_BKT_CAP_SCALE"]
+    assert got == want
+
+
+def test_bucket_ceiling_window(gpu):
+    """Sparse buckets to p < 2^32 at the top of the number line."""
+    w = golden("ceiling.json")
+    recs = w["records"] if "records" in w else [w]
+    r = recs[0]
+    with gpu.Device(r.get("cover", (1 << 64) - 1)) as dev:
+        assert dev.bucket_info()["active"] == 1
+        got = dev.verify_segment(r["a"], r["b"]).as_dict()
+    for k in ("evens", "unverified", "sum_pmin", "pos_hash", "max_p", "max_n"):
+        assert got[k] == r[k], (k, got, r)
+
+
+def test_reference_api_conformance_gpu(gpu):
+    """The device-backed reference entry points (phase1_verify,
+    verify_segment, phase2_resolve, is_prime_u64, build_base_primes,
+    tiled_sieve_segment) through the reference signatures."""
+    import subprocess
+    from conftest import ROOT
+    exe = os.path.join(ROOT, "paper_2603_07850_b200", "bin", "ref_api_conformance")
+    out = subprocess.run([exe, "--gpu"], capture_output=True, text=True, timeout=300)
+    assert out.returncode == 0, out.stdout + out.stderr[-2000:]
+    assert "conformance ok" in out.stdout
