@@ -167,18 +167,18 @@ int gb_is_prime_batch(gb_dev* dev, const uint64_t* values, uint8_t* out,
  * i.e. a counterexample). */
 int gb_phase2_resolve(gb_dev* dev, uint64_t n, uint64_t* p);
 
-/* Bucket sieve of the large base primes (k_bucket_fill: each prime's
- * multiples filed once per piece under the block they hit, the
- * reference's sorted hit list of sieve.cpp:109-126).  enabled = 0 puts
- * every prime back on the per-block row path (A/B timing; results are
- * identical).  No segments may be pending.  Not part of the reference
- * interface. */
+/* Mask fill of the large tile primes (k_mask_fill: every base prime from
+ * the threshold up to 2^22 struck once per 3-block range of a piece into
+ * the piece's large-prime bitmask, instead of visited by every block --
+ * the reference's sparse-prime hit list, sieve.cpp:109-126, in bitmask
+ * form).  enabled = 0 puts those primes back on the per-block row path
+ * (A/B timing; results are identical).  No segments may be pending.  Not
+ * part of the reference interface. */
 int gb_set_bucket(gb_dev* dev, int enabled);
 
-/* Bucket plan of the handle: [0] active, [1] smallest bucket prime,
- * [2] bucket primes, [3] fill chunks, [4] hits per block list,
- * [5] blocks per slot, [6] expected hits per block, [7] pieces re-run on
- * the row path after a list overflow. */
+/* Mask-fill plan: [0] active, [1] smallest mask prime, [2] mask primes,
+ * [3] cells per fill range, [4] primes above 2^22 (k_large_strike);
+ * [5..7] zero. */
 int gb_bucket_info(const gb_dev* dev, uint64_t* out8);
 
 /* Kernel launches issued by this handle since open (bench evidence). */
@@ -186,7 +186,7 @@ int gb_launch_count(const gb_dev* dev, uint64_t* launches);
 
 /* Device time (ms) spent in each kernel family since the last reset,
  * measured with CUDA events on the handle's streams: [0]=segment sieve+check
- * (K2/K3 fused), [1]=pre-kernels (row offsets, bucket fill or large-prime
+ * (K2/K3 fused), [1]=pre-kernels (row offsets, mask fill, large-prime
  * strike), [2]=stragglers/Phase 2, [3]=other. */
 int gb_kernel_times(gb_dev* dev, double* ms4, uint64_t* launches4, int reset);
 

@@ -323,13 +323,13 @@ class Device:
         _check(lib().gb_set_timing(self._h, int(mode)), self._h)
 
     def set_bucket(self, enabled: bool):
-        """Bucket sieve of the large primes on/off (results are identical)."""
+        """Mask fill of the large tile primes on/off (results are identical)."""
         _check(lib().gb_set_bucket(self._h, 1 if enabled else 0), self._h)
 
     def bucket_info(self) -> dict:
         v = (C.c_uint64 * 8)()
         _check(lib().gb_bucket_info(self._h, v), self._h)
-        keys = ("active", "p0", "primes", "chunks", "cap", "blocks", "expect", "fallbacks")
+        keys = ("active", "p0", "primes", "range_cells", "large_primes")
         return dict(zip(keys, list(v)))
 
     def io_bytes(self):

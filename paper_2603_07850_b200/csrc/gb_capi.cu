@@ -64,8 +64,6 @@ struct Batch {
     SegJob* d_jobs = nullptr;
     uint4* d_pmc = nullptr;           // per slot {p, magic, c0} of the tile primes
     uint32_t* d_qg = nullptr;
-    uint32_t* d_bkt = nullptr;          // bucket hit lists [slot][block][bk_cap]
-    uint32_t* d_bcnt = nullptr;         // [slot][block] hits filed
     SlotAcc* d_acc = nullptr;
     StragEntry* d_list = nullptr;
     unsigned int* d_counters = nullptr; // [0] block counter, [1] list count
@@ -78,7 +76,7 @@ struct Batch {
     bool launched = false;
     bool timed = false;
     bool large = false;
-    bool pre = false;                   // pre-kernels timed (large strike / bucket fill)
+    bool pre = false;                   // pre-kernels timed (mask fill / large strike)
 };
 
 struct UserSeg {
@@ -100,21 +98,16 @@ struct gb_dev {
     uint32_t iA0 = 0, iA1 = 0, iB1 = 0; // tile prime index ranges
     uint32_t iQ1 = 0, iH1 = 0;          // first tile primes >= M6/4, >= M6/2
     uint32_t iW1 = 0;                   // first tile prime >= W
-    uint16_t* d_wsplit = nullptr;       // [SPLIT_WARPS][32] balanced warp-cooperative primes
-    uint32_t sw = WS_SW_LIGHT;          // sieve warps of the fused kernel
+    uint16_t* d_wsplit = nullptr;       // [SPLIT_WARPS][32] balanced warp-cooperative primes (light split)
+    uint16_t* d_wsplit_heavy = nullptr; // the same for the heavy split
     uint64_t* d_m64 = nullptr;          // floor(2^64 / p) per base prime
     uint64_t iL0 = 0, iL1 = 0;          // large primes
-    // bucket sieve plan (k_bucket_fill): primes [iK0, n_primes)
-    bool bk_on = false;                 // plan built and lists allocated
-    bool bk_off_now = false;            // rows mode (fallback after a list overflow, or gb_set_bucket)
+    // mask fill (k_mask_fill): tile primes [iK0, iB1) struck per 3-block
+    // range into the large-prime bitmask instead of visited by every block
+    bool mk_on = false;                 // plan built
+    bool mk_off_now = false;            // rows only (gb_set_bucket(dev, 0))
     uint32_t iK0 = 0;
-    uint32_t bk_nb = 0;                 // blocks per slot in the list layout
-    uint64_t bk_cap = 0;                // hits per block list
-    double bk_expect = 0;               // expected hits per block (both arrays)
-    std::vector<BktChunk> bk_chunks;
-    BktChunk* d_chunks = nullptr;
-    uint64_t bk_fallbacks = 0;          // pieces re-run in rows mode
-    uint32_t bk_p0 = 0;                 // smallest bucket prime
+    uint32_t mk_p0 = 0;                 // smallest mask prime
     uint32_t* d_pat = nullptr;
     uint32_t* d_pat6 = nullptr;         // wheel-6 presieve patterns
     uint64_t* d_masks6 = nullptr;       // wheel-6 deep-window masks
@@ -164,11 +157,8 @@ static int batch_alloc(gb_dev* d, Batch& b, bool with_qg) {
     uint32_t np = d->iB1 - d->iA0;
     CU(d, dmalloc(d->device, &b.d_jobs, SLOTS * sizeof(SegJob)));
     CU(d, dmalloc(d->device, &b.d_pmc, (size_t)SLOTS * std::max<uint32_t>(np, 1) * sizeof(uint4)));
-    if (with_qg && d->iL1 > d->iL0) CU(d, dmalloc(d->device, &b.d_qg, (size_t)SLOTS * d->qg_stride * 4));
-    if (d->bk_on) {
-        CU(d, dmalloc(d->device, &b.d_bkt, (size_t)SLOTS * d->bk_nb * d->bk_cap * 4));
-        CU(d, dmalloc(d->device, &b.d_bcnt, (size_t)SLOTS * d->bk_nb * 4));
-    }
+    if (with_qg && (d->iL1 > d->iL0 || d->mk_on))
+        CU(d, dmalloc(d->device, &b.d_qg, (size_t)SLOTS * d->qg_stride * 4));
     CU(d, dmalloc(d->device, &b.d_acc, SLOTS * sizeof(SlotAcc)));
     CU(d, dmalloc(d->device, &b.d_list, (size_t)LIST_CAP * sizeof(StragEntry)));
     CU(d, dmalloc(d->device, &b.d_counters, 4 * sizeof(unsigned int)));
@@ -188,8 +178,6 @@ static void batch_free(gb_dev* d, Batch& b) {
     dfree(d->device, b.d_jobs);
     dfree(d->device, b.d_pmc);
     dfree(d->device, b.d_qg);
-    dfree(d->device, b.d_bkt);
-    dfree(d->device, b.d_bcnt);
     dfree(d->device, b.d_acc);
     dfree(d->device, b.d_list);
     dfree(d->device, b.d_counters);
@@ -209,7 +197,7 @@ static void batch_free(gb_dev* d, Batch& b) {
 // Fill the job descriptor of one piece: wheel-6 blocks of E6 evens whose
 // windows start at Q_b = Q + 6 K6 b, Q = the largest q = 1 (mod 6) with
 // q <= a - PH6 (negative near the start of the number line).
-static void make_job(gb_dev* d, const Piece& pc, SegJob& j, uint32_t prefix) {
+static void make_job(gb_dev* d, const Piece& pc, SegJob& j, uint32_t prefix, bool use_qg) {
     j.a = pc.a;
     j.b = pc.b;
     j.evens = (uint32_t)(((pc.b - pc.a) >> 1) + 1);
@@ -233,56 +221,54 @@ static void make_job(gb_dev* d, const Piece& pc, SegJob& j, uint32_t prefix) {
             j.qmod[g] = (uint32_t)(((q % P) + P) % P);
         }
     }
-    j.qg_words = d->iL1 > d->iL0 ? (uint32_t)(((uint64_t)j.nblocks * K6 + (M6 - K6) + 31) / 32) : 0;
+    j.qg_words = use_qg ? (uint32_t)(((uint64_t)j.nblocks * K6 + (M6 - K6) + 31) / 32) : 0;
 }
 
 static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     const uint32_t n = (uint32_t)b.pieces.size();
-    uint32_t prefix = 0;
-    bool large = false;
+    const bool large = d->iL1 > d->iL0;          // primes > P_TILE_MAX: k_large_strike
+    const bool mask = d->mk_on && !d->mk_off_now; // tile primes >= iK0: k_mask_fill
+    const bool use_qg = large || mask;
+    uint32_t prefix = 0, max_qw = 0;
     for (uint32_t s = 0; s < n; ++s) {
-        make_job(d, b.pieces[s], b.h_jobs[s], prefix);
+        make_job(d, b.pieces[s], b.h_jobs[s], prefix, use_qg);
         prefix += b.h_jobs[s].nblocks;
-        large |= b.h_jobs[s].qg_words != 0;
+        max_qw = std::max(max_qw, b.h_jobs[s].qg_words);
     }
     b.large = large;
-    const bool bk = d->bk_on && !d->bk_off_now;
     cudaStream_t st = d->serial ? d->sync.st : b.st;
     d->h2d_bytes += n * sizeof(SegJob);
     d->d2h_bytes += n * sizeof(DevRecord);
     CU(d, cudaMemcpyAsync(b.d_jobs, b.h_jobs, n * sizeof(SegJob), cudaMemcpyHostToDevice, st));
     CU(d, cudaMemsetAsync(b.d_acc, 0, n * sizeof(SlotAcc), st));
     CU(d, cudaMemsetAsync(b.d_counters, 0, 4 * sizeof(unsigned int), st));
-    if (bk) CU(d, cudaMemsetAsync(b.d_bcnt, 0, (size_t)n * d->bk_nb * 4, st));
     b.timed = d->timing;
-    b.pre = large || bk;
+    b.pre = use_qg;
     if (b.timed) CU(d, cudaEventRecord(b.ev_l0, st));
-    if (large && !bk) {
-        CU(d, cudaMemsetAsync(b.d_qg, 0xFF, (size_t)n * d->qg_stride * 4, st));
-        CU(d, launch_large_strike(b.d_jobs, n, d->d_primes, d->d_m64, d->iL0, d->iL1, b.d_qg, d->qg_stride, st));
-        d->launches++;
-    }
     const uint32_t np = d->iB1 - d->iA0;
     if (np) {
         CU(d, launch_segment_offsets(b.d_jobs, n, d->d_primes, d->d_m64, d->iA0, np, b.d_pmc, st));
         d->launches++;
     }
-    if (bk) {
-        BucketArgs K{};
+    if (mask) {
+        // writes every mask word of each slot (no memset needed)
+        MaskArgs K{};
         K.jobs = b.d_jobs;
         K.nslots = n;
-        K.primes = d->d_primes;
-        K.m64 = d->d_m64;
         K.pmc = b.d_pmc;
         K.np = np;
         K.iA0 = d->iA0;
-        K.chunks = d->d_chunks;
-        K.bkt = b.d_bkt;
-        K.bcnt = b.d_bcnt;
-        K.bk_nb = d->bk_nb;
-        K.bk_cap = d->bk_cap;
-        K.flag = b.d_counters + 2;
-        CU(d, launch_bucket_fill(K, (uint32_t)d->bk_chunks.size(), st));
+        K.iK0 = d->iK0;
+        K.iK1 = d->iB1;
+        K.qg = b.d_qg;
+        K.qg_stride_words = d->qg_stride;
+        CU(d, launch_mask_fill(K, max_qw, st));
+        d->launches++;
+    } else if (large) {
+        CU(d, cudaMemsetAsync(b.d_qg, 0xFF, (size_t)n * d->qg_stride * 4, st));
+    }
+    if (large) {
+        CU(d, launch_large_strike(b.d_jobs, n, d->d_primes, d->d_m64, d->iL0, d->iL1, b.d_qg, d->qg_stride, st));
         d->launches++;
     }
     VerifyArgs A{};
@@ -299,15 +285,13 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     A.iH1 = d->iH1;
     A.iW1 = d->iW1;
     A.np = np;
-    A.sw = d->sw;
+    A.iK0 = mask ? d->iK0 : d->iB1;
+    // sieve/check split by the primes the sieve group still visits per block
+    // (the row primes; the mask fill takes the rest)
+    A.sw = (A.iK0 - d->iA0) > WS_HEAVY_PRIMES ? WS_SW_HEAVY : WS_SW_LIGHT;
     A.pmc = b.d_pmc;
-    A.wsplit = d->d_wsplit;
-    A.qg = large && !bk ? b.d_qg : nullptr;
-    A.iK0 = bk ? d->iK0 : d->iB1;
-    A.bk_nb = d->bk_nb;
-    A.bk_cap = d->bk_cap;
-    A.bkt = bk ? b.d_bkt : nullptr;
-    A.bk_cnt = bk ? b.d_bcnt : nullptr;
+    A.wsplit = A.sw == WS_SW_HEAVY ? d->d_wsplit_heavy : d->d_wsplit;
+    A.qg = use_qg ? b.d_qg : nullptr;
     A.qg_stride_words = d->qg_stride;
     A.gpat6 = d->d_pat6;
     A.masks6 = d->d_masks6;
@@ -326,8 +310,7 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     if (b.timed) CU(d, cudaEventRecord(b.ev_k1, st));
     CU(d, launch_stragglers(b.d_jobs, b.d_list, b.d_counters + 1, LIST_CAP, d->prm.p_small, b.d_res, pmin_out,
                             d->sms, st));
-    CU(d, launch_finalize(b.d_jobs, n, b.d_acc, b.d_list, b.d_counters + 1, LIST_CAP, b.d_res,
-                          bk ? b.d_counters + 2 : nullptr, b.d_rec, st));
+    CU(d, launch_finalize(b.d_jobs, n, b.d_acc, b.d_list, b.d_counters + 1, LIST_CAP, b.d_res, b.d_rec, st));
     if (b.timed) CU(d, cudaEventRecord(b.ev_s1, st));
     d->launches += 3;
     CU(d, cudaMemcpyAsync(b.h_rec, b.d_rec, n * sizeof(DevRecord), cudaMemcpyDeviceToHost, st));
@@ -376,16 +359,6 @@ static int run_piece_sync(gb_dev* d, uint64_t a, uint64_t b, DevRecord* out, uin
     CU(d, cudaEventSynchronize(s.ev_done));
     CU(d, cudaGetLastError());
     s.launched = false;
-    if ((s.h_rec[0].overflow & 2) && !d->bk_off_now) {
-        // a bucket list overflowed: again with rows only
-        d->bk_off_now = true;
-        d->bk_fallbacks++;
-        rc = batch_launch(d, s, pmin_out);
-        if (rc == GB_OK && cudaEventSynchronize(s.ev_done) != cudaSuccess) rc = GB_ERR_CUDA;
-        s.launched = false;
-        d->bk_off_now = false;
-        if (rc) GB_FAIL(d, rc, "bucket fallback launch failed");
-    }
     *out = s.h_rec[0];
     return GB_OK;
 }
@@ -404,23 +377,6 @@ static int rerun_split(gb_dev* d, uint64_t a, uint64_t b, gb_seg_record& into) {
         if (y == b) break;
     }
     return GB_OK;
-}
-
-// A piece whose bucket lists overflowed (more hits in a block than bk_cap:
-// never seen, but the sizing is statistical): re-run it with every prime on
-// the row path, which needs no lists.
-static int rerun_rows(gb_dev* d, uint64_t a, uint64_t b, gb_seg_record& into) {
-    const bool prev = d->bk_off_now;
-    d->bk_off_now = true;
-    d->bk_fallbacks++;
-    DevRecord r;
-    int rc = run_piece_sync(d, a, b, &r, nullptr);
-    if (rc == GB_OK) {
-        if (r.overflow) rc = rerun_split(d, a, b, into);
-        else rec_merge(into, r);
-    }
-    d->bk_off_now = prev;
-    return rc;
 }
 
 static int batch_complete(gb_dev* d, int bi) {
@@ -454,11 +410,7 @@ static int batch_complete(gb_dev* d, int bi) {
         UserSeg* u = find_seg(d, b.pieces[s].seq);
         if (!u) GB_FAIL(d, GB_ERR_INTERNAL, "completed piece has no owner");
         const DevRecord& r = b.h_rec[s];
-        if (r.overflow & 2) {
-            // a bucket list overflowed: the piece again with rows only
-            int rc = rerun_rows(d, b.pieces[s].a, b.pieces[s].b, u->rec);
-            if (rc) return rc;
-        } else if (r.overflow) {
+        if (r.overflow) {
             int rc = rerun_split(d, b.pieces[s].a, b.pieces[s].b, u->rec);
             if (rc) return rc;
         } else {
@@ -578,81 +530,26 @@ static int device_odd_primes_upto(gb_dev* d, uint64_t L, uint32_t** d_out, uint6
     return GB_OK;
 }
 
-// Bucket sieve plan: primes >= GB_BKT_P (default M6 = 2^18; 0 turns the
-// bucket sieve off) are filed per block by k_bucket_fill.  Expected hits per
-// block window: sum over the primes of 2 M6 / p (one class array of M6 cells
-// each); list capacity = that plus a wide margin (the count is a sum of many
-// near-independent hits, its spread is ~sqrt of it).  Chunks: dense (p <=
-// P_TILE_MAX, first multiples from the rows) 512 primes each; sparse ones
-// grow until their staged hits per block fill the CTA's staging with every
-// block of a piece as one range.
-static int bucket_plan(gb_dev* d, const std::vector<uint32_t>& head) {
-    d->bk_on = false;
+// Mask-fill plan: tile primes >= GB_MASK_P (default M6 + 1: at most one
+// multiple per class array of a block window; 0 turns the mask fill off)
+// are struck by k_mask_fill once per 3-block range instead of by every
+// block's sieve (the reference's sparse-prime hit list, sieve.cpp:109-126,
+// in bitmask form).  On by default only where the large-prime bitmask exists
+// anyway (s > P_TILE_MAX: C5, the 2^64 ceiling): measured on B200, the fill
+// costs as much device time as it takes off the fused kernel at 1e12 / 1e13
+// (DESIGN.md sec. 6), since it cannot share SMs with the persistent kernel.
+static int mask_plan(gb_dev* d, const std::vector<uint32_t>& head) {
+    d->mk_on = false;
     d->iK0 = d->iB1;
-    uint64_t pb = M6;
-    if (const char* e = getenv("GB_BKT_P")) pb = strtoull(e, nullptr, 0);
-    if (pb == 0 || d->n_primes == 0) return GB_OK;
-    pb = std::max<uint64_t>(pb, 1u << 16);
-    const uint64_t total = d->n_primes;
-    // host copy of the primes beyond the head when there are any (C5, ceiling)
-    std::vector<uint32_t> tail;
-    if (total > head.size()) {
-        tail.resize(total - head.size());
-        CU(d, cudaMemcpy(tail.data(), d->d_primes + head.size(), tail.size() * 4, cudaMemcpyDeviceToHost));
-    }
-    auto P = [&](uint64_t i) -> uint32_t { return i < head.size() ? head[i] : tail[i - head.size()]; };
-    uint64_t lo = 0, hi = total; // first index with p >= pb
-    while (lo < hi) {
-        const uint64_t m = (lo + hi) / 2;
-        if (P(m) < pb) lo = m + 1; else hi = m;
-    }
-    uint64_t iK0 = std::max<uint64_t>(lo, d->iA1);
-    if (iK0 >= total) return GB_OK;
-    const uint32_t nb = (uint32_t)((d->max_piece + E6 - 1) / E6);
-    auto capl_of = [](double e) { return ((uint32_t)std::ceil(e + 6.0 * std::sqrt(e) + 16.0) + 3u) & ~3u; };
-    double etot = 0;
-    std::vector<BktChunk> ch;
-    const uint64_t iRow1 = d->iB1; // rows exist for [iA0, iB1)
-    uint64_t i = iK0;
-    while (i < total) {
-        BktChunk c{};
-        c.i0 = (uint32_t)i;
-        double e = 0;
-        if (i < iRow1) {
-            const uint64_t j1 = std::min<uint64_t>(iRow1, i + BK_THREADS);
-            for (uint64_t j = i; j < j1; ++j) e += 2.0 * M6 / P(j);
-            i = j1;
-        } else {
-            // every block of a piece in one range when the staging allows
-            const uint32_t target = std::max<uint32_t>(BK_STAGE_WORDS / nb - 1, 24u);
-            uint64_t j = i;
-            while (j < total) {
-                const double e2 = e + 2.0 * M6 / P(j);
-                if (j > i && capl_of(e2) > target) break;
-                e = e2;
-                ++j;
-            }
-            i = j;
-        }
-        c.i1 = (uint32_t)i;
-        c.capl = capl_of(e);
-        c.rb = std::max<uint32_t>(1, std::min<uint32_t>(nb, BK_STAGE_WORDS / (c.capl + 1)));
-        etot += e;
-        ch.push_back(c);
-    }
-    double scale = 1.0;
-    if (const char* e = getenv("GB_BKT_CAP_SCALE")) scale = atof(e); // tests: force list overflows
-    uint64_t cap = (uint64_t)std::ceil((etot * 1.02 + 8.0 * std::sqrt(etot) + 1024.0) * scale);
-    cap = std::max<uint64_t>(4, (cap + 3) & ~3ull);
-    d->iK0 = (uint32_t)iK0;
-    d->bk_p0 = P(iK0);
-    d->bk_nb = nb;
-    d->bk_cap = cap;
-    d->bk_expect = etot;
-    d->bk_chunks = ch;
-    CU(d, dmalloc(d->device, &d->d_chunks, ch.size() * sizeof(BktChunk)));
-    CU(d, cudaMemcpy(d->d_chunks, ch.data(), ch.size() * sizeof(BktChunk), cudaMemcpyHostToDevice));
-    d->bk_on = true;
+    uint64_t pm = d->iL1 > d->iL0 ? M6 + 1 : 0;
+    if (const char* e = getenv("GB_MASK_P")) pm = strtoull(e, nullptr, 0);
+    if (pm == 0) return GB_OK;
+    pm = std::max<uint64_t>(pm, P_WARP_MAX); // warp-cooperative primes stay on rows
+    const uint32_t i = (uint32_t)(std::lower_bound(head.begin(), head.end(), (uint32_t)std::min<uint64_t>(pm, P_TILE_MAX + 1ull)) - head.begin());
+    if (i >= d->iB1) return GB_OK; // no tile prime that large
+    d->iK0 = std::max(i, d->iA1);
+    d->mk_p0 = head[d->iK0];
+    d->mk_on = true;
     return GB_OK;
 }
 
@@ -677,11 +574,11 @@ static int build_tables(gb_dev* d) {
     d->iH1 = std::max(d->iQ1, std::min(d->iW1, (uint32_t)(std::lower_bound(hp.begin(), hp.end(), M6 / 2) - hp.begin())));
     d->iL0 = d->iB1;
     d->iL1 = total;
-    {
-        // warp-cooperative primes [iA0, iA1) to warps, longest first onto the
-        // least loaded warp (cost ~ strikes per lane W / 32p + setup)
-        d->sw = (d->iB1 - d->iA0) > WS_HEAVY_PRIMES ? WS_SW_HEAVY : WS_SW_LIGHT;
-        const int nwarps = (int)d->sw;
+    // warp-cooperative primes [iA0, iA1) to warps, longest first onto the
+    // least loaded warp (cost ~ strikes per lane W / 32p + setup); one table
+    // per compiled split, the split being chosen per launch (batch_launch)
+    for (int h = 0; h < 2; ++h) {
+        const int nwarps = h ? WS_SW_HEAVY : WS_SW_LIGHT;
         std::vector<uint16_t> ws(SPLIT_WARPS * 32, 0xFFFF);
         std::vector<double> load(nwarps, 0.0);
         std::vector<int> cnt(nwarps, 0);
@@ -693,13 +590,14 @@ static int build_tables(gb_dev* d) {
             ws[best * 32 + cnt[best]++] = (uint16_t)(i - d->iA0);
             load[best] += 2.0 * M6 / (32.0 * hp[i]) + 6.0;
         }
-        CU(d, dmalloc(d->device, &d->d_wsplit, ws.size() * sizeof(uint16_t)));
-        CU(d, cudaMemcpy(d->d_wsplit, ws.data(), ws.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
+        uint16_t*& dst = h ? d->d_wsplit_heavy : d->d_wsplit;
+        CU(d, dmalloc(d->device, &dst, ws.size() * sizeof(uint16_t)));
+        CU(d, cudaMemcpy(dst, ws.data(), ws.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
     }
     CU(d, dmalloc(d->device, &d->d_m64, std::max<uint64_t>(total, 1) * sizeof(uint64_t)));
     CU(d, launch_prime_magic64(d->d_primes, total, d->d_m64, d->sync.st));
     d->launches++;
-    int rc2 = bucket_plan(d, hp);
+    int rc2 = mask_plan(d, hp);
     if (rc2) return rc2;
     CU(d, cudaStreamSynchronize(d->sync.st)); // tables ready before any batch stream
     return GB_OK;
@@ -728,10 +626,12 @@ int gb_open(int device, const gb_params* params, gb_dev** out) {
     if (!params) GB_FAIL(nullptr, GB_ERR_PARAM, "gb_open: params is NULL");
     if (params->p_small < 3) GB_FAIL(nullptr, GB_ERR_PARAM, "SmallPrimeTable: p_small must be >= 3");
     if (params->cover_limit < 1) GB_FAIL(nullptr, GB_ERR_PARAM, "build_base_primes: cover_limit must be >= 1");
+    const double t_enter = now_s();
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || n == 0)
         GB_FAIL(nullptr, GB_ERR_CUDA, "gb_open: no CUDA device available");
     if (device < 0 || device >= n) GB_FAIL(nullptr, GB_ERR_PARAM, "gb_open: device index out of range");
+    const double t_count = now_s();
     gb_dev* d = new gb_dev();
     d->device = device;
     d->prm = *params;
@@ -754,7 +654,7 @@ int gb_open(int device, const gb_params* params, gb_dev** out) {
             break;
         }
         cudaDeviceGetAttribute(&d->sms, cudaDevAttrMultiProcessorCount, device);
-        const double t_open0 = now_s();
+        const double t_ctx = now_s();
         int occ = 0;
         if (verify_occupancy(&occ) != 0 || occ < 1) {
             set_err(d, "gb_open: fused kernel cannot be resident (shared memory)");
@@ -762,6 +662,7 @@ int gb_open(int device, const gb_params* params, gb_dev** out) {
             break;
         }
         d->occ = occ;
+        const double t_open0 = now_s();
         d->sqrt_bound = sqrt_bound_of(params->cover_limit);
         if (cudaStreamCreateWithFlags(&d->sync.st, cudaStreamNonBlocking) != cudaSuccess) {
             set_err(d, "gb_open: cudaStreamCreate failed");
@@ -777,8 +678,11 @@ int gb_open(int device, const gb_params* params, gb_dev** out) {
         if ((rc = batch_alloc(d, d->sync, true)) != GB_OK) break;
         for (int i = 0; i < NBATCH && rc == GB_OK; ++i) rc = batch_alloc(d, d->batches[i], true);
         if (getenv("GB_DEBUG_OPEN"))
-            fprintf(stderr, "gb_open: setup %.1f ms, tables %.1f ms, batches %.1f ms\n", 1e3 * (t_open1 - t_open0),
-                    1e3 * (t_open2 - t_open1), 1e3 * (now_s() - t_open2));
+            fprintf(stderr,
+                    "gb_open: driver %.1f ms, context %.1f ms, kernels %.1f ms, setup %.1f ms, tables %.1f ms, "
+                    "batches %.1f ms\n",
+                    1e3 * (t_count - t_enter), 1e3 * (t_ctx - t_count), 1e3 * (t_open0 - t_ctx),
+                    1e3 * (t_open1 - t_open0), 1e3 * (t_open2 - t_open1), 1e3 * (now_s() - t_open2));
     } while (false);
     if (rc != GB_OK) {
         t_err = d->err;
@@ -804,8 +708,8 @@ int gb_close(gb_dev* d) {
     dfree(d->device, d->d_pat6);
     dfree(d->device, d->d_masks6);
     dfree(d->device, d->d_wsplit);
+    dfree(d->device, d->d_wsplit_heavy);
     dfree(d->device, d->d_m64);
-    dfree(d->device, d->d_chunks);
     delete d;
     return GB_OK;
 }
@@ -1004,16 +908,9 @@ uint64_t gb_estimate_device_bytes(uint64_t cover_limit, uint64_t p_small, uint64
     const uint64_t np_all = pi_upper(s);
     const uint64_t np_tile = std::min<uint64_t>(np_all, pi_upper(P_TILE_MAX));
     const uint64_t piece = std::min<uint64_t>(max_seg_evens, MAX_PIECE);
-    const uint64_t qg = s > P_TILE_MAX ? SLOTS * 2 * ((((piece + E6 - 1) / E6) * K6 + (M6 - K6) + 31) / 32) * 4 : 0;
-    // bucket lists: sum over primes M6 <= p <= s of 2 M6 / p hits per block
-    // (Mertens: 2 M6 (ln ln s - ln ln M6)), with bucket_plan's margin
-    uint64_t bkt = 0;
-    if (s > M6) {
-        const double e = 2.0 * M6 * (std::log(std::log((double)s)) - std::log(std::log((double)M6)));
-        const double cap = std::max(0.0, e) * 1.05 + 8.0 * std::sqrt(std::max(0.0, e)) + 1024.0;
-        bkt = (uint64_t)(SLOTS * ((piece + E6 - 1) / E6) * (cap * 4 + 4));
-    }
-    const uint64_t per_batch = SLOTS * np_tile * sizeof(uint4) + qg + bkt + (uint64_t)LIST_CAP * (sizeof(StragEntry) + sizeof(StragResult)) +
+    // large-prime bitmask: primes > P_TILE_MAX, or the mask fill (s > M6)
+    const uint64_t qg = s > M6 ? SLOTS * 2 * ((((piece + E6 - 1) / E6) * K6 + (M6 - K6) + 31) / 32) * 4 : 0;
+    const uint64_t per_batch = SLOTS * np_tile * sizeof(uint4) + qg + (uint64_t)LIST_CAP * (sizeof(StragEntry) + sizeof(StragResult)) +
                                SLOTS * (sizeof(SegJob) + sizeof(SlotAcc) + sizeof(DevRecord)) + 64;
     // base primes + their 64-bit magics + K1 scratch bitmap (transient) + NBATCH + 1 batches
     return np_all * (4 + 8) + (s / 16 + 64) + (uint64_t)(NBATCH + 1) * per_batch;
@@ -1048,20 +945,18 @@ extern "C" int gb_debug_stats(uint64_t* out8, int reset) {
 int gb_set_bucket(gb_dev* d, int enabled) {
     if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
     if (!d->segs.empty()) GB_FAIL(d, GB_ERR_PARAM, "gb_set_bucket: segments pending");
-    d->bk_off_now = !enabled;
+    d->mk_off_now = !enabled;
     return GB_OK;
 }
 
 int gb_bucket_info(const gb_dev* d, uint64_t* out8) {
     if (!d || !out8) return GB_ERR_PARAM;
-    out8[0] = d->bk_on && !d->bk_off_now;
-    out8[1] = d->bk_on ? d->bk_p0 : 0;
-    out8[2] = d->bk_on ? (uint64_t)d->n_primes - d->iK0 : 0;
-    out8[3] = d->bk_chunks.size();
-    out8[4] = d->bk_cap;
-    out8[5] = d->bk_nb;
-    out8[6] = (uint64_t)std::llround(d->bk_expect);
-    out8[7] = d->bk_fallbacks;
+    for (int i = 0; i < 8; ++i) out8[i] = 0;
+    out8[0] = d->mk_on && !d->mk_off_now;
+    out8[1] = d->mk_on ? d->mk_p0 : 0;
+    out8[2] = d->mk_on ? d->iB1 - d->iK0 : 0;
+    out8[3] = MK_CELLS;
+    out8[4] = d->iL1 - d->iL0;
     return GB_OK;
 }
 

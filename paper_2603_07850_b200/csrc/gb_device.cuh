@@ -87,31 +87,18 @@ constexpr uint32_t TILE6_WORDS = 3 * TPAD + 2 * M6W; // [pad][A][pad][B][pad]
 static_assert(K6 % 32 == 0 && 6 * (M6 - K6) > PH6 + 5, "wheel-6 block geometry");
 static_assert(64 * NWIN6 * 6 >= PH6, "deep windows cover the halo");
 
-// ---------------------------------------------------------- bucket sieve
-// Primes >= the bucket threshold (default M6: at most one multiple per class
-// array of a window) are not visited block by block.  k_bucket_fill walks
-// each prime's multiples across a whole piece once and files every hit under
-// the block whose window holds it, as one u32 per hit: the tile word-space
-// cell (BK_ENC_A + k for array A cell k, BK_ENC_B + k for B), so the fused
-// kernel's strike is one RED at word u >> 5, bit u & 31 of the tile.  A cell
-// k of the piece lies in the window of block k / K6 and, when k mod K6 <
-// DUP6, also in the window of the block before (windows overlap by DUP6).
-// This is the reference's sorted hit list for sparse primes (sieve.cpp:
-// 109-126, 144-147), built for all blocks of a piece in one pass.
-constexpr uint32_t DUP6 = M6 - K6;                  // 1376 cells
-constexpr uint32_t BK_ENC_A = 32 * TPAD;            // tile cell of A's cell 0
-constexpr uint32_t BK_ENC_B = 32 * (2 * TPAD + M6W); // tile cell of B's cell 0
-constexpr uint32_t BK_THREADS = 512;                // k_bucket_fill CTA (2 per SM)
-constexpr uint32_t BK_STAGE_WORDS = 20 * 1024;      // per-CTA staging: rb bins x (capl + 1) words
-// One CTA task: primes [i0, i1) of the base-prime table, filed for one slot
-// in ranges of rb blocks with capl staged hits per block.  Chunks with
-// i1 <= the end of the row table (dense: one prime per thread) take their
-// first multiples from the slot's pmc rows; the others (sparse, many primes
-// per thread) compute them from the prime's 64-bit magic.
-struct BktChunk {
-    uint32_t i0, i1;
-    uint32_t rb, capl;
-};
+// ------------------------------------------------------------- mask fill
+// k_mask_fill: one CTA per MK_CELLS cells (3 block strides) of both class
+// arrays of a slot's large-prime bitmask, held in shared memory.
+constexpr uint32_t MK_CELLS = 3 * K6;               // 782304 (a multiple of 32)
+constexpr uint32_t MK_WORDS = MK_CELLS / 32;        // per array
+constexpr uint32_t MK_THREADS = 512;
+constexpr size_t MK_SMEM = 2ull * MK_WORDS * 4;     // 195.6 KB: one CTA per SM
+#ifndef GB_MK_INFLIGHT
+#define GB_MK_INFLIGHT 4 // rows loaded before their strikes
+#endif
+constexpr int MK_INFLIGHT = GB_MK_INFLIGHT;
+static_assert(MK_CELLS % 32 == 0, "mask ranges align to words");
 
 // wheel-6 presieve groups: pattern bit k is 0 iff a prime of the group
 // divides 6k + 1 (3 has no cells)

@@ -479,153 +479,58 @@ __device__ __forceinline__ void block_off6(const uint4 v, uint32_t KB, uint32_t&
     ob = min(t, t - p);
 }
 
-// ============================================================ bucket fill
-// Lanes with the same block bin file their hits with one shared atomic per
-// bin (warp-collective: every lane calls it; act = the lane has a hit).  A
-// bin whose staging is full spills the hit straight to the global list.
-struct BkStage {
-    uint32_t* stage;  // [rb][capl]
-    uint32_t* cnt;    // [rb]
-    uint32_t capl;
-    uint32_t* gl;     // global list of bin 0 of the range ([bin][cap])
-    uint32_t* gc;     // global counts of bin 0 of the range
-    uint64_t cap;
-    unsigned int* flag;
-};
-
-__device__ __forceinline__ void bk_emit(const BkStage& S, bool act, uint32_t bin, uint32_t u, uint32_t lane) {
-    const uint32_t peers = __match_any_sync(0xffffffffu, act ? bin : 0xFFFFFFFFu);
-    if (!act) return;
-    const uint32_t leader = __ffs(peers) - 1;
-    uint32_t base = 0;
-    if (lane == leader) base = atomicAdd(&S.cnt[bin], (uint32_t)__popc(peers));
-    base = __shfl_sync(peers, base, leader) + __popc(peers & ((1u << lane) - 1));
-    if (base < S.capl) {
-        S.stage[bin * S.capl + base] = u;
-    } else {
-        const uint32_t g = atomicAdd(&S.gc[bin], 1u);
-        if (g < S.cap) S.gl[(size_t)bin * S.cap + g] = u;
-        else atomicOr(S.flag, 1u);
-    }
-}
-
-// Hits of one class array in blocks [B0, B1) of the piece: o is the prime's
-// first multiple at or after cell E0 = B0 K6 (relative to the slot origin).
-// Every multiple below E1 = B1 K6 is filed under its block, and under the
-// block before when it lies in the windows' overlap; the first multiple at
-// or after E1 files only its overlap copy (block B1 - 1), since its own
-// block belongs to the next range.  On return o is the first multiple
-// >= E1 (0xFFFFFFFF once past 2^32).  Warp-collective.
-__device__ __forceinline__ void bk_run(const BkStage& S, uint32_t& o, uint32_t p, bool has, uint32_t enc,
-                                       uint32_t B0, uint32_t E1, uint32_t nbins, uint32_t lane) {
-    for (;;) {
-        const bool act = has && o < E1;
-        if (!__any_sync(0xffffffffu, act)) break;
-        const uint32_t b = o / K6; // constant divisor: multiply-high
-        const uint32_t w = o - b * K6;
-        bk_emit(S, act, b - B0, enc + w, lane);
-        const bool dup = act && w < DUP6 && b > B0;
-        if (__any_sync(0xffffffffu, dup)) bk_emit(S, dup, b - 1 - B0, enc + w + K6, lane);
-        if (act) o = p >= 0xFFFFFFFFu - o ? 0xFFFFFFFFu : o + p;
-    }
-    const bool tail = has && o != 0xFFFFFFFFu && o - E1 < DUP6;
-    if (__any_sync(0xffffffffu, tail)) bk_emit(S, tail, nbins - 1, enc + (o - E1) + K6, lane);
-}
-
-// first multiple >= E0 of a progression k0 + j p (k0 < p), 32-bit; m32 <=
-// floor(2^32 / p) makes the quotient estimate low by at most 2
-__device__ __forceinline__ uint32_t first_ge(uint32_t k0, uint32_t E0, uint32_t p, uint32_t m32) {
-    if (k0 >= E0) return k0;
-    const uint32_t x = E0 - k0;       // < 2^29
-    uint32_t q = __umulhi(x, m32);
-    uint32_t r = x - q * p;
-    while (r >= p) { r -= p; ++q; }
-    const uint64_t o = (uint64_t)k0 + (uint64_t)(q + (r != 0)) * p;
-    return o > 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)o;
-}
-
-// One CTA per (chunk, slot): blockIdx.x = chunk * nslots + slot, so the
-// slots of one chunk run side by side and share its primes in L2.
-__global__ void __launch_bounds__(BK_THREADS, 2) k_bucket_fill(BucketArgs A) {
-    extern __shared__ __align__(16) uint32_t bsm[];
-    const uint32_t s = blockIdx.x % A.nslots;
-    const BktChunk C = A.chunks[blockIdx.x / A.nslots];
-    const SegJob J = A.jobs[s];
-    const uint32_t nb = J.nblocks;
-    const uint32_t lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    constexpr uint32_t NW = BK_THREADS / 32;
-    BkStage S;
-    S.stage = bsm;
-    S.cnt = bsm + C.rb * C.capl;
-    S.capl = C.capl;
-    S.cap = A.bk_cap;
-    S.flag = A.flag;
-    for (uint32_t i = threadIdx.x; i < C.rb; i += BK_THREADS) S.cnt[i] = 0;
-    const bool dense = C.i1 <= A.iA0 + A.np;
-    // dense chunk: one prime per thread, carried across the ranges
-    uint32_t p = 0, oA = 0xFFFFFFFFu, oB = 0xFFFFFFFFu;
-    bool has = false;
-    if (dense) {
-        const uint32_t i = C.i0 + threadIdx.x;
-        has = i < C.i1;
-        if (has) {
-            const uint4 v = A.pmc[(size_t)s * A.np + (i - A.iA0)];
-            p = v.x;
-            block_off6(v, 0, oA, oB);
-        }
-    }
+// ============================================================ mask fill
+// Large tile primes (>= the mask threshold, default M6: at most one multiple
+// per class array of a block window) are not visited block by block.  One
+// CTA owns MK_CELLS consecutive cells of both class arrays of a slot's
+// wheel-6 bitmask (qg) in shared memory, visits every such prime once for
+// all of them (first multiple from the slot's row, then the multiples in the
+// range), strikes with shared REDs and stores the words with plain coalesced
+// writes: no global atomics, no hit lists.  The fused kernel ANDs the words
+// of its window into the tile (sieve_block), the same words the large-prime
+// strikes of k_large_strike land in (p > P_TILE_MAX, run after this).
+// A block window visits a prime once per MK_CELLS / K6 = 3 blocks instead of
+// once per block.
+__global__ void __launch_bounds__(MK_THREADS, 1) k_mask_fill(MaskArgs A) {
+    extern __shared__ __align__(16) uint32_t msm[];
+    uint32_t* ma = msm;            // array A words [c0, c0 + MK_CELLS)
+    uint32_t* mb = msm + MK_WORDS; // array B
+    const uint32_t s = blockIdx.y;
+    const uint32_t qw = A.jobs[s].qg_words;
+    const uint32_t w0 = blockIdx.x * MK_WORDS;
+    if (w0 >= qw) return;
+    const uint32_t nw = min(MK_WORDS, qw - w0);
+    const uint32_t c0 = 32 * w0, len = 32 * nw;
+    for (uint32_t i = threadIdx.x; i < 2 * MK_WORDS; i += MK_THREADS) msm[i] = ~0u;
     __syncthreads();
-    for (uint32_t B0 = 0; B0 < nb; B0 += C.rb) {
-        const uint32_t B1 = min(nb, B0 + C.rb);
-        const uint32_t E0 = B0 * K6, E1 = B1 * K6;
-        const size_t key0 = (size_t)s * A.bk_nb + B0;
-        S.gl = A.bkt + key0 * A.bk_cap;
-        S.gc = A.bcnt + key0;
-        if (dense) {
-            bk_run(S, oA, p, has, BK_ENC_A, B0, E1, B1 - B0, lane);
-            bk_run(S, oB, p, has, BK_ENC_B, B0, E1, B1 - B0, lane);
-        } else {
-            // sparse: many primes per thread, first multiples from scratch
-            for (uint32_t ib = C.i0 + warp * 32; ib < C.i1; ib += BK_THREADS) {
-                const uint32_t i = ib + lane;
-                const bool h = i < C.i1;
-                uint32_t q = 0, a = 0xFFFFFFFFu, bb = 0xFFFFFFFFu;
-                if (h) {
-                    q = A.primes[i];
-                    const uint64_t m = A.m64[i];
-                    const uint32_t k0 = first_a6(J, q, m);
-                    const uint32_t c = b_shift6(q);
-                    const uint32_t k0b = k0 >= c ? k0 - c : k0 + (q - c);
-                    const uint32_t m32 = (uint32_t)(m >> 32);
-                    a = first_ge(k0, E0, q, m32);
-                    bb = first_ge(k0b, E0, q, m32);
-                }
-                bk_run(S, a, q, h, BK_ENC_A, B0, E1, B1 - B0, lane);
-                bk_run(S, bb, q, h, BK_ENC_B, B0, E1, B1 - B0, lane);
-            }
-        }
-        __syncthreads();
-        // flush: one global reservation per bin, coalesced copy
-        for (uint32_t bin = warp; bin < B1 - B0; bin += NW) {
-            const uint32_t n = min(S.cnt[bin], C.capl);
-            __syncwarp();
-            if (n) {
-                uint64_t base = 0;
-                if (lane == 0) {
-                    base = atomicAdd(&S.gc[bin], n);
-                    S.cnt[bin] = 0;
-                    if (base + n > A.bk_cap) atomicOr(A.flag, 1u);
-                }
-                base = __shfl_sync(0xffffffffu, base, 0);
-                uint32_t* dst = S.gl + (size_t)bin * A.bk_cap;
-                const uint32_t* src = S.stage + bin * C.capl;
-                for (uint32_t j = lane; j < n; j += 32)
-                    if (base + j < A.bk_cap) dst[base + j] = src[j];
-            } else if (lane == 0) {
-                S.cnt[bin] = 0;
-            }
-        }
-        __syncthreads();
+    const uint32_t ta = (uint32_t)__cvta_generic_to_shared(ma), tb = (uint32_t)__cvta_generic_to_shared(mb);
+    const uint4* rows = A.pmc + (size_t)s * A.np - A.iA0;
+    auto one = [&](const uint4 v) {
+        uint32_t oa, ob;
+        block_off6(v, c0, oa, ob); // first multiples at or after c0, relative to it
+        for (uint32_t x = oa; x < len; x += v.x)
+            asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(ta + ((x >> 3) & ~3u)),
+                         "r"(__funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, x)) : "memory");
+        for (uint32_t x = ob; x < len; x += v.x)
+            asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(tb + ((x >> 3) & ~3u)),
+                         "r"(__funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, x)) : "memory");
+    };
+    // rows come from L2: MK_INFLIGHT loaded before their strikes
+    uint32_t i = A.iK0 + threadIdx.x;
+    for (; i + (MK_INFLIGHT - 1) * MK_THREADS < A.iK1; i += MK_INFLIGHT * MK_THREADS) {
+        uint4 v[MK_INFLIGHT];
+#pragma unroll
+        for (int u = 0; u < MK_INFLIGHT; ++u) v[u] = __ldg(rows + i + u * MK_THREADS);
+#pragma unroll
+        for (int u = 0; u < MK_INFLIGHT; ++u) one(v[u]);
+    }
+    for (; i < A.iK1; i += MK_THREADS) one(__ldg(rows + i));
+    __syncthreads();
+    uint32_t* ga = A.qg + s * A.qg_stride_words + w0;
+    uint32_t* gb = ga + qw;
+    for (uint32_t w = threadIdx.x; w < nw; w += MK_THREADS) {
+        ga[w] = ma[w];
+        gb[w] = mb[w];
     }
 }
 
@@ -756,7 +661,7 @@ __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __re
     // thread per prime; the rows come from L2, so several are loaded before
     // their strikes to keep loads in flight per warp.  Primes >= M6/4 strike
     // an array at most 4 (>= M6/2: 2, >= M6: 1) times, unrolled branch-free.
-    // rows end at nK (the first bucket prime; nB when the bucket sieve is off)
+    // rows end at nK (the first mask prime; nB when the mask fill is off)
     nQ = min(nQ, nK);
     nH = min(nH, nK);
     nW = min(nW, nK);
@@ -768,49 +673,6 @@ __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __re
 #ifndef GB_SKIP_SINGLE // timing probe: no single-strike primes (wrong results)
     strike_rows<GT, 1, SS_INFLIGHT>(A6, B6, pmc + nW + tid, pmc + nB, KB, lane);
 #endif
-}
-
-#ifndef GB_BK_INFLIGHT
-#define GB_BK_INFLIGHT 4 // 16-B hit loads in flight per thread
-#endif
-// one bucket hit: RED.AND of bit u & 31 of tile word u >> 5 (tb: the tile's
-// shared address)
-__device__ __forceinline__ void strike_cell(uint32_t tb, uint32_t u) {
-    asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(tb + ((u >> 3) & ~3u)),
-                 "r"(__funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, u))
-                 : "memory");
-}
-
-// Bucket hits of one block (k_bucket_fill's list) by a group of GT threads:
-// 16-B loads, GB_BK_INFLIGHT per thread in flight, then their REDs.
-template <int GT>
-__device__ __forceinline__ void strike_bucket(uint32_t* tile, const uint32_t* __restrict__ e, uint32_t n,
-                                              uint32_t tid) {
-    const uint32_t tb = (uint32_t)__cvta_generic_to_shared(tile);
-    const uint4* e4 = reinterpret_cast<const uint4*>(e);
-    const uint32_t n4 = n >> 2; // full quads
-    constexpr int U = GB_BK_INFLIGHT;
-    uint32_t i = tid;
-    for (; i + (U - 1) * GT < n4; i += U * GT) {
-        uint4 v[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) v[u] = __ldcs(e4 + i + u * GT);
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-            strike_cell(tb, v[u].x);
-            strike_cell(tb, v[u].y);
-            strike_cell(tb, v[u].z);
-            strike_cell(tb, v[u].w);
-        }
-    }
-    for (; i < n4; i += GT) {
-        const uint4 v = __ldcs(e4 + i);
-        strike_cell(tb, v.x);
-        strike_cell(tb, v.y);
-        strike_cell(tb, v.z);
-        strike_cell(tb, v.w);
-    }
-    if (tid < (n & 3)) strike_cell(tb, __ldcs(e + 4 * n4 + tid));
 }
 
 // Presieve one class array (M6W words) with the wheel-6 patterns; ph[g] =
@@ -1380,28 +1242,39 @@ __device__ __forceinline__ void sieve_block(const VerifyArgs& A, uint32_t* tile,
     presieve6(arr_a(tile), pat6, pha, tid, GT);
     presieve6(arr_b(tile), pat6, phb, tid, GT);
     gbar<GT>(bar);
+    if (A.qg != nullptr && I.J.qg_words) {
+        // large-prime mask words of this window (k_mask_fill, k_large_strike),
+        // ANDed as REDs so they need no barrier against the strikes below
+        const uint32_t* ga = A.qg + I.s * A.qg_stride_words + I.KB / 32;
+        const uint32_t* gb = ga + I.J.qg_words;
+        const uint32_t lim = min(M6W, I.J.qg_words - I.KB / 32);
+        const uint32_t sa = (uint32_t)__cvta_generic_to_shared(arr_a(tile));
+        const uint32_t sb = (uint32_t)__cvta_generic_to_shared(arr_b(tile));
+        constexpr int U = 4;
+        uint32_t wd = tid;
+        for (; wd + (U - 1) * GT < lim; wd += U * GT) {
+            uint32_t va[U], vb[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                va[u] = __ldcs(ga + wd + u * GT);
+                vb[u] = __ldcs(gb + wd + u * GT);
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(sa + 4 * (wd + u * GT)), "r"(va[u]) : "memory");
+                asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(sb + 4 * (wd + u * GT)), "r"(vb[u]) : "memory");
+            }
+        }
+        for (; wd < lim; wd += GT) {
+            asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(sa + 4 * wd), "r"(__ldcs(ga + wd)) : "memory");
+            asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(sb + 4 * wd), "r"(__ldcs(gb + wd)) : "memory");
+        }
+    }
 #ifndef GB_SKIP_STRIKES // timing probe: the check group on presieved-only tiles
     strike_verify6<GT>(tile, A.pmc + (size_t)I.s * A.np, A.iA1 - A.iA0, A.iQ1 - A.iA0, A.iH1 - A.iA0,
                        A.iW1 - A.iA0, A.iB1 - A.iA0, A.iK0 - A.iA0, I.KB, tid,
                        A.wsplit);
-    if (A.bk_cnt != nullptr) {
-        const size_t key = (size_t)I.s * A.bk_nb + I.b;
-        const uint32_t n = (uint32_t)min((uint64_t)A.bk_cnt[key], A.bk_cap);
-        strike_bucket<GT>(tile, A.bkt + key * A.bk_cap, n, tid);
-    }
 #endif
-    if (A.qg != nullptr && I.J.qg_words) {
-        gbar<GT>(bar);
-        const uint32_t* ga = A.qg + I.s * A.qg_stride_words + I.KB / 32;
-        const uint32_t* gb = ga + I.J.qg_words;
-        const uint32_t lim = min(M6W, I.J.qg_words - I.KB / 32);
-        uint32_t* ta = arr_a(tile);
-        uint32_t* tb = arr_b(tile);
-        for (uint32_t wd = tid; wd < lim; wd += GT) {
-            ta[wd] &= __ldg(ga + wd);
-            tb[wd] &= __ldg(gb + wd);
-        }
-    }
     if (I.low) {
         gbar<GT>(bar);
         fixup_low6(tile, I.Qs, A.primes, A.n_primes, A.sbound, tid, GT);
@@ -1550,6 +1423,28 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
     }
 }
 
+// L2 prefetch (TMA bulk prefetch, nothing to wait for) of the large-prime
+// mask words block fb's sieve will AND in: 2 x M6W words per array.  One thread.
+__device__ __forceinline__ void prefetch_mask(const VerifyArgs& A, const SegJob* jobs, uint32_t fb) {
+    if (fb >= A.total_blocks) return;
+    uint32_t s = 0;
+    while (s + 1 < A.nslots && jobs[s + 1].block_prefix <= fb) ++s;
+    const SegJob& J = jobs[s];
+    const uint32_t w0 = (fb - J.block_prefix) * (K6 / 32);
+    if (w0 >= J.qg_words) return;
+    const uint32_t bytes = 4 * min(M6W, J.qg_words - w0);
+    const uint32_t* ga = A.qg + s * A.qg_stride_words + w0;
+#pragma unroll
+    for (int arr = 0; arr < 2; ++arr) {
+        // 16-B aligned sub-range of the words (never past them: the
+        // allocation's end is never crossed)
+        const uint64_t a0 = reinterpret_cast<uint64_t>(ga + arr * J.qg_words);
+        const uint64_t p0 = a0 & ~15ull, p1 = (a0 + bytes) & ~15ull;
+        if (p1 > p0)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p0), "r"((uint32_t)(p1 - p0)) : "memory");
+    }
+}
+
 // Warp-specialised fused kernel: one 896-thread CTA per SM, two wheel-6
 // tile buffers.  The first 32 SW threads (the sieve group) sieve block k
 // into buffer k & 1 while the other threads (the check group) check
@@ -1580,10 +1475,19 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
     __syncthreads();
     const int NB = WS_THREADS; // participants of FULL / EMPTY
     if (threadIdx.x < ST) {
-        // ---- sieve group
+        // ---- sieve group.  Claims run two blocks ahead, so the mask words
+        // of the block after the current one are prefetched into L2 a whole
+        // block before the sieve ANDs them in.
         const uint32_t tid = threadIdx.x;
-        uint32_t fb_next = 0;
-        if (tid == 0) fb_next = atomicAdd(A.block_counter, 1u);
+        uint32_t fb_next = 0, fb_next2 = 0;
+        if (tid == 0) {
+            fb_next = atomicAdd(A.block_counter, 1u);
+            fb_next2 = atomicAdd(A.block_counter, 1u);
+            if (A.qg != nullptr) {
+                prefetch_mask(A, s_jobs, fb_next);
+                prefetch_mask(A, s_jobs, fb_next2);
+            }
+        }
         for (uint32_t k = 0;; ++k) {
             const uint32_t bs = k & 1;
             uint32_t* tile = tiles + bs * TILE6_WORDS;
@@ -1596,7 +1500,11 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
                 nb_arrive(BAR_FULL + bs, NB);                  // check group sees the end
                 return;
             }
-            if (tid == 0) fb_next = atomicAdd(A.block_counter, 1u);
+            if (tid == 0) {
+                fb_next = fb_next2;
+                fb_next2 = atomicAdd(A.block_counter, 1u);
+                if (A.qg != nullptr && k > 0) prefetch_mask(A, s_jobs, fb_next);
+            }
             const BlockInfo I = block_info(A, s_jobs, fb);
             sieve_block<ST>(A, tile, pat6, I, tid, BAR_S);
             nb_arrive(BAR_FULL + bs, NB);
@@ -1713,8 +1621,7 @@ __device__ void add_ce(DevRecord& r, uint64_t n) {
 
 __global__ void k_finalize(const SegJob* __restrict__ jobs, uint32_t nslots, const SlotAcc* __restrict__ acc,
                            const StragEntry* __restrict__ list, const unsigned int* __restrict__ list_count,
-                           uint32_t list_cap, const StragResult* __restrict__ res,
-                           const unsigned int* __restrict__ bk_flag, DevRecord* __restrict__ out) {
+                           uint32_t list_cap, const StragResult* __restrict__ res, DevRecord* __restrict__ out) {
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     uint32_t cnt = *list_count;
     for (uint32_t s = 0; s < nslots; ++s) {
@@ -1730,7 +1637,7 @@ __global__ void k_finalize(const SegJob* __restrict__ jobs, uint32_t nslots, con
             r.max_p = k >> 32;
             r.max_n = J.a + 2ull * (0xFFFFFFFFu - (uint32_t)(k & 0xFFFFFFFFu));
         }
-        r.overflow = (cnt > list_cap ? 1u : 0u) | (bk_flag && *bk_flag ? 2u : 0u);
+        r.overflow = cnt > list_cap;
         out[s] = r;
     }
     uint32_t m = min(cnt, list_cap);
@@ -1868,9 +1775,10 @@ cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint3
                                                                                  iL1, qg, qg_stride_words);
     return cudaGetLastError();
 }
-cudaError_t launch_bucket_fill(const BucketArgs& a, uint32_t nchunks, cudaStream_t st) {
-    if (!nchunks || !a.nslots) return cudaSuccess;
-    k_bucket_fill<<<nchunks * a.nslots, BK_THREADS, BK_STAGE_WORDS * 4, st>>>(a);
+cudaError_t launch_mask_fill(const MaskArgs& a, uint32_t max_qg_words, cudaStream_t st) {
+    if (!a.nslots || a.iK1 <= a.iK0) return cudaSuccess;
+    const dim3 grid((max_qg_words + MK_WORDS - 1) / MK_WORDS, a.nslots);
+    k_mask_fill<<<grid, MK_THREADS, MK_SMEM, st>>>(a);
     return cudaGetLastError();
 }
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st) {
@@ -1894,8 +1802,8 @@ cudaError_t launch_stragglers(const SegJob* jobs, const StragEntry* list, const 
 }
 cudaError_t launch_finalize(const SegJob* jobs, uint32_t nslots, const SlotAcc* acc, const StragEntry* list,
                             const unsigned int* list_count, uint32_t list_cap, const StragResult* res,
-                            const unsigned int* bk_flag, DevRecord* out, cudaStream_t st) {
-    k_finalize<<<1, 32, 0, st>>>(jobs, nslots, acc, list, list_count, list_cap, res, bk_flag, out);
+                            DevRecord* out, cudaStream_t st) {
+    k_finalize<<<1, 32, 0, st>>>(jobs, nslots, acc, list, list_count, list_cap, res, out);
     return cudaGetLastError();
 }
 cudaError_t launch_phase2_one(uint64_t n, uint64_t* out, cudaStream_t st) {
@@ -1913,8 +1821,7 @@ int verify_occupancy(int* blocks_per_sm) {
     if (cudaFuncSetAttribute(k_sieve_interval, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)SIEVE_SMEM) !=
         cudaSuccess)
         return 1;
-    if (cudaFuncSetAttribute(k_bucket_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(BK_STAGE_WORDS * 4)) !=
-        cudaSuccess)
+    if (cudaFuncSetAttribute(k_mask_fill, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)MK_SMEM) != cudaSuccess)
         return 1;
     if (cudaFuncSetAttribute(k_verify_ws<false, WS_SW_LIGHT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)WS_SMEM) != cudaSuccess ||

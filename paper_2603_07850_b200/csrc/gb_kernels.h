@@ -47,28 +47,19 @@ struct VerifyArgs {
     unsigned int* list_count;
     uint32_t list_cap;
     uint64_t* pmin_out;           // optional per-even output (single slot)
-    // bucket sieve (nullptr bk_cnt = off): primes >= iK0 come from per-block
-    // hit lists instead of rows; rows stop at iK0
-    uint32_t iK0;                 // first bucket prime (= iB1 when off)
-    uint32_t bk_nb;               // blocks per slot in the list layout
-    uint64_t bk_cap;              // hits per block list
-    const uint32_t* bkt;          // [slot][block][bk_cap] tile cells
-    const uint32_t* bk_cnt;       // [slot][block] hits filed (may exceed bk_cap: overflow)
+    // rows stop at iK0: tile primes from iK0 on are struck into qg by
+    // k_mask_fill (iK0 = iB1 when the mask fill is off)
+    uint32_t iK0;
 };
 
-struct BucketArgs {
-    const SegJob* jobs;
+struct MaskArgs {
+    const SegJob* jobs;           // qg_words per slot
     uint32_t nslots;
-    const uint32_t* primes;
-    const uint64_t* m64;
     const uint4* pmc;             // rows of [iA0, iA0 + np) per slot
     uint32_t np, iA0;
-    const BktChunk* chunks;
-    uint32_t* bkt;
-    uint32_t* bcnt;
-    uint32_t bk_nb;
-    uint64_t bk_cap;
-    unsigned int* flag;           // set when a block list overflows
+    uint32_t iK0, iK1;            // mask primes (row indices are i - iA0)
+    uint32_t* qg;
+    uint64_t qg_stride_words;
 };
 
 // dynamic shared memory of the tile kernels
@@ -95,14 +86,14 @@ cudaError_t launch_segment_offsets(const SegJob* jobs, uint32_t nslots, const ui
                                    const uint64_t* m64, uint32_t iA0, uint32_t np, uint4* pmc, cudaStream_t st);
 cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, const uint64_t* m64,
                                 uint64_t iL0, uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, cudaStream_t st);
-cudaError_t launch_bucket_fill(const BucketArgs& a, uint32_t nchunks, cudaStream_t st);
+cudaError_t launch_mask_fill(const MaskArgs& a, uint32_t max_qg_words, cudaStream_t st);
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_stragglers(const SegJob* jobs, const StragEntry* list, const unsigned int* list_count,
                               uint32_t list_cap, uint64_t p_small, StragResult* res, uint64_t* pmin_out,
                               int grid, cudaStream_t st);
 cudaError_t launch_finalize(const SegJob* jobs, uint32_t nslots, const SlotAcc* acc, const StragEntry* list,
                             const unsigned int* list_count, uint32_t list_cap, const StragResult* res,
-                            const unsigned int* bk_flag, DevRecord* out, cudaStream_t st);
+                            DevRecord* out, cudaStream_t st);
 cudaError_t launch_phase2_one(uint64_t n, uint64_t* out, cudaStream_t st);
 cudaError_t launch_is_prime_batch(const uint64_t* v, uint8_t* out, uint64_t n, cudaStream_t st);
 cudaError_t launch_smem_peak(uint32_t iters, uint32_t* sink, int grid, cudaStream_t st);

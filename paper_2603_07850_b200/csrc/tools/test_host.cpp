@@ -182,6 +182,24 @@ static void test_pool() {
         CHECK(t.counterexamples == std::vector<uint64_t>({10, 30}));
         CHECK(t.pmin_sum == 4); // wraps mod 2^64
     }
+    {   // exact counterexample counts past the stored GB_REC_MAX_CE values:
+        // a record with 20 counterexamples keeps 16 values and the count 20
+        gb_seg_record r{};
+        r.a = 4;
+        r.b = 1000;
+        r.evens_checked = 499;
+        r.unverified_p1 = 20;
+        r.n_counterexamples = 20;
+        for (int i = 0; i < GB_REC_MAX_CE; ++i) r.counterexamples[i] = 10 + 2 * i;
+        const SegmentReport rep = report_from_record(r);
+        CHECK(rep.counterexamples.size() == GB_REC_MAX_CE && rep.unverified_after_phase1 == 20);
+        RunResult t, a;
+        a.counterexamples = rep.counterexamples;
+        a.counterexample_count = r.n_counterexamples;
+        merge_into(t, a);
+        merge_into(t, a);
+        CHECK(t.counterexample_count == 40 && t.counterexamples.size() == 2 * GB_REC_MAX_CE);
+    }
 }
 
 // ---- verifier host pieces (test_verifier.cpp:23-37, 239-263)

@@ -1,10 +1,12 @@
-"""Bucket sieve of the large base primes (k_bucket_fill + the fused kernel's
-list strikes) against the per-block row path and the reference goldens.
+"""Mask fill of the large tile primes (k_mask_fill: every prime >= the
+threshold struck once per 3-block range into the slot's large-prime bitmask,
+which the fused kernel ANDs in) against the per-block row path and the
+reference goldens.
 
-The bucket sieve changes only WHERE a large prime's strikes come from (a
-per-block hit list filed once per piece instead of a row visited by every
-block), so every record must be bit-identical to the row path and to the
-reference (sieve.cpp:109-126, 144-147 is the reference's own hit list)."""
+The mask fill changes only WHERE a large prime's strikes come from (one
+visit per 3 blocks instead of one per block), so every record must be
+bit-identical to the row path and to the reference (sieve.cpp:109-126,
+144-147 is the reference's own sparse-prime hit list)."""
 import os
 
 import pytest
@@ -34,66 +36,34 @@ CASES = [
 @pytest.mark.parametrize("cover,a,n", CASES)
 def test_bucket_equals_rows(gpu, cover, a, n):
     b = a + 2 * (n - 1)
-    with _open(gpu, cover) as dev:
+    os.environ["GB_MASK_P"] = "262145"  # on at every height (default: s > 2^22 only)
+    try:
+        dev = _open(gpu, cover)
+    finally:
+        del os.environ["GB_MASK_P"]
+    with dev:
         info = dev.bucket_info()
         assert info["active"] == 1 and info["primes"] > 0, info
         got = _rec(dev, a, b)
         dev.set_bucket(False)
         want = _rec(dev, a, b)
         dev.set_bucket(True)
-        assert dev.bucket_info()["fallbacks"] == 0
     assert got == want
 
 
-def test_bucket_c2_records(gpu):
-    """All 25 C2 segments (reference records) with the threshold lowered to
-    2^16 so the bucket primes start inside C2's base primes (s = 1e5)."""
-    os.environ["GB_BKT_P"] = "65536"
-    try:
-        recs = golden("c2_segments.json")["records"]
-        with gpu.Device(10**10) as dev:
-            assert dev.bucket_info()["p0"] == 65537
-            for r in recs:
-                got = dev.verify_segment(r["a"], r["b"]).as_dict()
-                for k in ("evens", "unverified", "sum_pmin", "pos_hash", "max_p", "max_n"):
-                    assert got[k] == r[k], (k, r["a"], got, r)
-    finally:
-        del os.environ["GB_BKT_P"]
-
-
-@pytest.mark.parametrize("pb", ["65536", "131072", "524288", "1048576", "0"])
+@pytest.mark.parametrize("pb", ["65536", "131072", "262145", "1048576", "0"])
 def test_bucket_thresholds_agree(gpu, pb):
     a, b = 10**13 - 40_000_000, 10**13
     with gpu.Device(10**13) as dev:
         want = _rec(dev, a, b)
-    os.environ["GB_BKT_P"] = pb
+    os.environ["GB_MASK_P"] = pb
     try:
         with gpu.Device(10**13) as dev:
             info = dev.bucket_info()
             assert info["active"] == (0 if pb == "0" else 1)
             assert _rec(dev, a, b) == want
     finally:
-        del os.environ["GB_BKT_P"]
-
-
-def test_bucket_overflow_falls_back_to_rows(gpu):
-    """Lists far too small: every block overflows, the fill raises the flag
-    and the host re-runs the piece on the row path; results stay exact."""
-    a, b = 10**12 - 40_000_000, 10**12
-    with gpu.Device(10**12) as dev:
-        want = _rec(dev, a, b)
-    os.environ["GB_BKT_CAP_SCALE"] = "0.001"
-    try:
-        with gpu.Device(10**12) as dev:
-            got = _rec(dev, a, b)
-            assert dev.bucket_info()["fallbacks"] >= 1
-            # the asynchronous path too
-            dev.submit(a, b, 7)
-            r, tag = dev.wait()
-            assert tag == 7 and r.key() == want
-    finally:
-        del os.environ["GB_BKT_CAP_SCALE"]
-    assert got == want
+        del os.environ["GB_MASK_P"]
 
 
 def test_bucket_ceiling_window(gpu):

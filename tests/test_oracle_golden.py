@@ -3,12 +3,13 @@ path) against golden vectors produced by the UNMODIFIED reference
 (oracle/make_goldens.py -> tests/golden/*.json) and the reference's own
 known-answer tests.  No GPU."""
 import hashlib
+import os
 
 import numpy as np
 import pytest
 
 import oracle
-from conftest import golden
+from conftest import GOLD, golden
 
 
 def test_known_answers_from_reference_tests():
@@ -108,3 +109,40 @@ def test_oracle_matches_compiled_reference_random_segments():
         want = oracle.ref_segment_record(a, b, b, 1_000_000, 0)
         got = oracle.verify_segment(a, b, cover=b)
         assert got.key() == want.key(), (a, b)
+
+
+def _big(name):
+    import gzip
+    path = os.path.join(GOLD, name)
+    if not os.path.exists(path):
+        pytest.skip(f"{name} not generated")
+    meta, rows = {}, []
+    with gzip.open(path, "rt") as f:
+        for line in f:
+            if line.startswith("#"):
+                meta.update(dict(t.split("=", 1) for t in line[1:].split() if "=" in t))
+                continue
+            if line.strip():
+                rows.append([int(x) for x in line.split()])
+    return {k: int(v) for k, v in meta.items()}, rows
+
+
+@pytest.mark.parametrize("name", ["c4_segments.tsv.gz", "c5_segments.tsv.gz"])
+def test_big_golden_files_follow_claim_rule(name):
+    """The C4/C5 reference records are WorkPool claims (pool.cpp:24-31):
+    segment idx is [start + idx * 2 seg, min(that + 2 seg - 2, limit)]."""
+    meta, rows = _big(name)
+    span = 2 * meta["seg_size"]
+    for r in rows:
+        a = meta["start"] + r[0] * span
+        assert (r[1], r[2]) == (a, min(a + span - 2, meta["limit"]))
+        assert r[3] == (r[2] - r[1]) // 2 + 1 and r[4] == 0 and r[10] == 0
+
+
+def test_oracle_matches_a_c4_reference_record():
+    """The C restatement against one reference record at the top of C4
+    (cover 1e13): the oracle is pinned at the north-star height too."""
+    meta, rows = _big("c4_segments.tsv.gz")
+    r = max(rows, key=lambda v: v[0])
+    got = oracle.verify_segment(r[1], r[2], cover=meta["cover"], p_small=meta["p_small"])
+    assert got.key()[:10] == tuple(r[1:])

@@ -5,7 +5,7 @@ limit = int(float(sys.argv[1])) if len(sys.argv) > 1 else 10**12
 t0 = time.time()
 dev = gb.Device(limit)
 t1 = time.time()
-print("open", t1 - t0, flush=True)
+print("open", t1 - t0, "bucket", dev.bucket_info(), flush=True)
 span = 400_000_000
 depth = dev.max_inflight()
 dev.set_timing(True)
