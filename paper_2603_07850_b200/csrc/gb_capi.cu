@@ -100,6 +100,7 @@ struct gb_dev {
     uint32_t iW1 = 0;                   // first tile prime >= W
     uint16_t* d_wsplit = nullptr;       // [SPLIT_WARPS][32] balanced warp-cooperative primes (light split)
     uint16_t* d_wsplit_heavy = nullptr; // the same for the heavy split
+    uint16_t* d_wsplit_mask = nullptr;  // and for the mask split
     uint64_t* d_m64 = nullptr;          // floor(2^64 / p) per base prime
     uint64_t iL0 = 0, iL1 = 0;          // large primes
     // mask fill (k_mask_fill): tile primes [iK0, iB1) struck per 3-block
@@ -108,6 +109,7 @@ struct gb_dev {
     bool mk_off_now = false;            // rows only (gb_set_bucket(dev, 0))
     uint32_t iK0 = 0;
     uint32_t mk_p0 = 0;                 // smallest mask prime
+    uint32_t force_sw = 0;              // GB_SW: force a compiled split (tuning)
     uint32_t* d_pat = nullptr;
     uint32_t* d_pat6 = nullptr;         // wheel-6 presieve patterns
     uint64_t* d_masks6 = nullptr;       // wheel-6 deep-window masks
@@ -288,9 +290,13 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     A.iK0 = mask ? d->iK0 : d->iB1;
     // sieve/check split by the primes the sieve group still visits per block
     // (the row primes; the mask fill takes the rest)
-    A.sw = (A.iK0 - d->iA0) > WS_HEAVY_PRIMES ? WS_SW_HEAVY : WS_SW_LIGHT;
+    // (more check warps above 2^44: p_min grows with n, the check with it;
+    // C5 window 0.183 s with 12 sieve warps against 0.189 s with 16)
+    const uint32_t rows = A.iK0 - d->iA0;
+    A.sw = rows > WS_HEAVY_PRIMES && !large ? WS_SW_HEAVY : rows > WS_MASK_PRIMES ? WS_SW_LIGHT : WS_SW_MASK;
+    if (d->force_sw) A.sw = d->force_sw;
     A.pmc = b.d_pmc;
-    A.wsplit = A.sw == WS_SW_HEAVY ? d->d_wsplit_heavy : d->d_wsplit;
+    A.wsplit = A.sw == WS_SW_HEAVY ? d->d_wsplit_heavy : A.sw == WS_SW_MASK ? d->d_wsplit_mask : d->d_wsplit;
     A.qg = use_qg ? b.d_qg : nullptr;
     A.qg_stride_words = d->qg_stride;
     A.gpat6 = d->d_pat6;
@@ -534,14 +540,19 @@ static int device_odd_primes_upto(gb_dev* d, uint64_t L, uint32_t** d_out, uint6
 // multiple per class array of a block window; 0 turns the mask fill off)
 // are struck by k_mask_fill once per 3-block range instead of by every
 // block's sieve (the reference's sparse-prime hit list, sieve.cpp:109-126,
-// in bitmask form).  On by default only where the large-prime bitmask exists
-// anyway (s > P_TILE_MAX: C5, the 2^64 ceiling): measured on B200, the fill
-// costs as much device time as it takes off the fused kernel at 1e12 / 1e13
-// (DESIGN.md sec. 6), since it cannot share SMs with the persistent kernel.
+// in bitmask form).  Off by default (GB_MASK_P=262145 turns it on): measured
+// on B200 the fill costs more device time than it takes off the fused kernel
+// at 1e12, 1e13 and the C5 window, because it cannot
+// share SMs with the persistent kernel while the row visits it replaces run
+// beside the check warps.
 static int mask_plan(gb_dev* d, const std::vector<uint32_t>& head) {
     d->mk_on = false;
     d->iK0 = d->iB1;
-    uint64_t pm = d->iL1 > d->iL0 ? M6 + 1 : 0;
+    if (const char* e = getenv("GB_SW")) {
+        const uint32_t v = (uint32_t)atoi(e);
+        if (v == WS_SW_LIGHT || v == WS_SW_HEAVY || v == WS_SW_MASK) d->force_sw = v;
+    }
+    uint64_t pm = 0;
     if (const char* e = getenv("GB_MASK_P")) pm = strtoull(e, nullptr, 0);
     if (pm == 0) return GB_OK;
     pm = std::max<uint64_t>(pm, P_WARP_MAX); // warp-cooperative primes stay on rows
@@ -577,8 +588,8 @@ static int build_tables(gb_dev* d) {
     // warp-cooperative primes [iA0, iA1) to warps, longest first onto the
     // least loaded warp (cost ~ strikes per lane W / 32p + setup); one table
     // per compiled split, the split being chosen per launch (batch_launch)
-    for (int h = 0; h < 2; ++h) {
-        const int nwarps = h ? WS_SW_HEAVY : WS_SW_LIGHT;
+    for (int h = 0; h < 3; ++h) {
+        const int nwarps = h == 0 ? WS_SW_LIGHT : h == 1 ? WS_SW_HEAVY : WS_SW_MASK;
         std::vector<uint16_t> ws(SPLIT_WARPS * 32, 0xFFFF);
         std::vector<double> load(nwarps, 0.0);
         std::vector<int> cnt(nwarps, 0);
@@ -590,7 +601,7 @@ static int build_tables(gb_dev* d) {
             ws[best * 32 + cnt[best]++] = (uint16_t)(i - d->iA0);
             load[best] += 2.0 * M6 / (32.0 * hp[i]) + 6.0;
         }
-        uint16_t*& dst = h ? d->d_wsplit_heavy : d->d_wsplit;
+        uint16_t*& dst = h == 0 ? d->d_wsplit : h == 1 ? d->d_wsplit_heavy : d->d_wsplit_mask;
         CU(d, dmalloc(d->device, &dst, ws.size() * sizeof(uint16_t)));
         CU(d, cudaMemcpy(dst, ws.data(), ws.size() * sizeof(uint16_t), cudaMemcpyHostToDevice));
     }
@@ -709,6 +720,7 @@ int gb_close(gb_dev* d) {
     dfree(d->device, d->d_masks6);
     dfree(d->device, d->d_wsplit);
     dfree(d->device, d->d_wsplit_heavy);
+    dfree(d->device, d->d_wsplit_mask);
     dfree(d->device, d->d_m64);
     delete d;
     return GB_OK;

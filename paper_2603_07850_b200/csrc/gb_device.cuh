@@ -30,12 +30,16 @@ constexpr int THREADS = 512;            // threads per CTA of k_sieve_interval
 #ifndef GB_WS_SW_HEAVY
 #define GB_WS_SW_HEAVY 16
 #endif
+#ifndef GB_WS_SW_MASK
+#define GB_WS_SW_MASK 10 // sieve warps when the mask fill takes the large primes
+#endif
 #ifndef GB_WS_THREADS
 #define GB_WS_THREADS 896
 #endif
 constexpr int WS_THREADS = GB_WS_THREADS;
-constexpr int WS_SW_LIGHT = GB_WS_SW_LIGHT, WS_SW_HEAVY = GB_WS_SW_HEAVY;
+constexpr int WS_SW_LIGHT = GB_WS_SW_LIGHT, WS_SW_HEAVY = GB_WS_SW_HEAVY, WS_SW_MASK = GB_WS_SW_MASK;
 constexpr uint32_t WS_HEAVY_PRIMES = 150000;
+constexpr uint32_t WS_MASK_PRIMES = 50000; // row primes at or below: the mask split
 // warps of the group that runs the warp-cooperative strikes (max of the splits)
 constexpr int SPLIT_WARPS = WS_SW_HEAVY > WS_SW_LIGHT ? WS_SW_HEAVY : WS_SW_LIGHT;
 constexpr uint32_t P_TILE_MAX = 1u << 22; // base primes above: K_large (global strikes)

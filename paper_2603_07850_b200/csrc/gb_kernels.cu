@@ -1788,6 +1788,9 @@ cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st)
     if (a.sw == WS_SW_HEAVY) {
         if (a.pmin_out) k_verify_ws<true, WS_SW_HEAVY><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
         else k_verify_ws<false, WS_SW_HEAVY><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
+    } else if (a.sw == WS_SW_MASK) {
+        if (a.pmin_out) k_verify_ws<true, WS_SW_MASK><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
+        else k_verify_ws<false, WS_SW_MASK><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
     } else {
         if (a.pmin_out) k_verify_ws<true, WS_SW_LIGHT><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
         else k_verify_ws<false, WS_SW_LIGHT><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
@@ -1830,6 +1833,11 @@ int verify_occupancy(int* blocks_per_sm) {
         cudaFuncSetAttribute(k_verify_ws<false, WS_SW_HEAVY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)WS_SMEM) != cudaSuccess ||
         cudaFuncSetAttribute(k_verify_ws<true, WS_SW_HEAVY>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)WS_SMEM) != cudaSuccess)
+        return 1;
+    if (cudaFuncSetAttribute(k_verify_ws<false, WS_SW_MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)WS_SMEM) != cudaSuccess ||
+        cudaFuncSetAttribute(k_verify_ws<true, WS_SW_MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                              (int)WS_SMEM) != cudaSuccess)
         return 1;
     int o1 = 0, o2 = 0;

@@ -36,7 +36,7 @@ CASES = [
 @pytest.mark.parametrize("cover,a,n", CASES)
 def test_bucket_equals_rows(gpu, cover, a, n):
     b = a + 2 * (n - 1)
-    os.environ["GB_MASK_P"] = "262145"  # on at every height (default: s > 2^22 only)
+    os.environ["GB_MASK_P"] = "262145"  # on (default: off)
     try:
         dev = _open(gpu, cover)
     finally:
@@ -71,7 +71,12 @@ def test_bucket_ceiling_window(gpu):
     w = golden("ceiling.json")
     recs = w["records"] if "records" in w else [w]
     r = recs[0]
-    with gpu.Device(r.get("cover", (1 << 64) - 1)) as dev:
+    os.environ["GB_MASK_P"] = "262145"
+    try:
+        dev = gpu.Device(r.get("cover", (1 << 64) - 1))
+    finally:
+        del os.environ["GB_MASK_P"]
+    with dev:
         assert dev.bucket_info()["active"] == 1
         got = dev.verify_segment(r["a"], r["b"]).as_dict()
     for k in ("evens", "unverified", "sum_pmin", "pos_hash", "max_p", "max_n"):
