@@ -5,6 +5,8 @@
 #include "goldbach/cli.hpp"
 
 #include <algorithm>
+#include <cstdlib>
+#include <chrono>
 #include <charconv>
 #include <cmath>
 #include <functional>
@@ -271,7 +273,12 @@ double efficiency(double t1, unsigned k, double tk) {
 
 int run(const Config& cfg, std::ostream& out, std::ostream& err) {
     Logger log(err);
+    // GB_DEBUG_OPEN: where a CLI process spends its time before and after the drain
+    const bool dbg = getenv("GB_DEBUG_OPEN") != nullptr;
+    const auto t_run = std::chrono::steady_clock::now();
+    auto since = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_run).count(); };
     const MemoryEstimate est = validate_resources(cfg);
+    if (dbg) log.logf("timing: validate_resources ", since(), " s");
     log.logf("memory estimate: ", human_bytes(est.total_bytes), " (", est.workers, " GPU worker(s) x ",
              human_bytes(est.per_worker_bytes), " + shared ", human_bytes(est.shared_bytes), ")");
     // tables are built on each GPU by its worker (K1); the host keeps only
@@ -290,6 +297,8 @@ int run(const Config& cfg, std::ostream& out, std::ostream& err) {
     opt.workers = est.workers;
     opt.progress = cfg.progress;
     const RunResult res = run_workers(pool, ctx, opt, log);
+    if (dbg) log.logf("timing: run_workers done ", since(), " s (worker init ", res.init_seconds, " s, wall ",
+                      res.wall_seconds, " s)");
     if (cfg.json)
         print_json(out, cfg, est.workers, res);
     else
