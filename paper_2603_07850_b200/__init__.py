@@ -150,6 +150,7 @@ def lib():
         "gb_kernel_times": ([vp, C.POINTER(C.c_double), p64, i32], i32),
         "gb_set_timing": ([vp, i32], i32),
         "gb_set_bucket": ([vp, i32], i32),
+        "gb_debug_tile": ([vp, u64, u64, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_int64)], i32),
         "gb_bucket_info": ([vp, p64], i32),
         "gb_io_bytes": ([vp, p64, p64], i32),
         "gb_flush_l2": ([vp], i32),
@@ -321,6 +322,17 @@ class Device:
     def set_timing(self, mode):
         """0/False off, 1/True event timing, 2 timing with serialised batches."""
         _check(lib().gb_set_timing(self._h, int(mode)), self._h)
+
+    def debug_tile(self, a: int, b: int, block: int):
+        """The fused kernel's sieved wheel-6 tile of one block (parity hook):
+        (origin Q, A words, B words); A bit k <-> q = Q + 6k, B bit k <->
+        q = Q + 4 + 6k."""
+        import numpy as np
+        w = np.zeros(2 * 8192, dtype=np.uint32)
+        q = C.c_int64()
+        _check(lib().gb_debug_tile(self._h, a, b, block, w.ctypes.data_as(C.POINTER(C.c_uint32)),
+                                   C.byref(q)), self._h)
+        return q.value, w[:8192], w[8192:]
 
     def set_bucket(self, enabled: bool):
         """Mask fill of the large tile primes on/off (results are identical)."""

@@ -10,6 +10,7 @@
 // CPU: host code only schedules, copies records and merges them
 // (MinPrimeMax / sums / counterexample lists, pool.cpp:159-174 semantics).
 #include <algorithm>
+#include <dlfcn.h>
 #include <chrono>
 #include <cmath>
 #include <cstdio>
@@ -226,7 +227,8 @@ static void make_job(gb_dev* d, const Piece& pc, SegJob& j, uint32_t prefix, boo
     j.qg_words = use_qg ? (uint32_t)(((uint64_t)j.nblocks * K6 + (M6 - K6) + 31) / 32) : 0;
 }
 
-static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
+static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out, uint32_t* tile_out = nullptr,
+                        uint32_t tile_fb = 0) {
     const uint32_t n = (uint32_t)b.pieces.size();
     const bool large = d->iL1 > d->iL0;          // primes > P_TILE_MAX: k_large_strike
     const bool mask = d->mk_on && !d->mk_off_now; // tile primes >= iK0: k_mask_fill
@@ -309,6 +311,8 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out) {
     A.list_count = b.d_counters + 1;
     A.list_cap = LIST_CAP;
     A.pmin_out = pmin_out;
+    A.tile_out = tile_out;
+    A.tile_fb = tile_fb;
     int grid = std::min<int>(d->sms * d->occ, (int)prefix);
     if (grid < 1) grid = 1;
     if (b.timed) CU(d, cudaEventRecord(b.ev_k0, st));
@@ -619,6 +623,38 @@ static uint64_t pi_upper(uint64_t x) { // Rosser-Schoenfeld style bound, sizing 
     return (uint64_t)(1.26 * (double)x / std::log((double)x)) + 1;
 }
 
+// NVML through dlopen (the driver ships libnvidia-ml.so.1; nothing is
+// linked at build time): free/total memory of a CUDA device, matched by PCI
+// bus id.  false when NVML is unavailable.
+static bool nvml_memory(int device, uint64_t* free_bytes, uint64_t* total_bytes) {
+    struct Mem {
+        unsigned long long total, free, used;
+    };
+    using InitFn = int (*)();
+    using ByPciFn = int (*)(const char*, void**);
+    using MemFn = int (*)(void*, Mem*);
+    static std::once_flag once;
+    static ByPciFn by_pci = nullptr;
+    static MemFn mem = nullptr;
+    std::call_once(once, [] {
+        void* h = dlopen("libnvidia-ml.so.1", RTLD_NOW | RTLD_LOCAL);
+        if (!h) return;
+        auto init = reinterpret_cast<InitFn>(dlsym(h, "nvmlInit_v2"));
+        by_pci = reinterpret_cast<ByPciFn>(dlsym(h, "nvmlDeviceGetHandleByPciBusId_v2"));
+        mem = reinterpret_cast<MemFn>(dlsym(h, "nvmlDeviceGetMemoryInfo"));
+        if (!init || !by_pci || !mem || init() != 0) by_pci = nullptr;
+    });
+    if (!by_pci) return false;
+    char bus[32] = {0};
+    if (cudaDeviceGetPCIBusId(bus, sizeof(bus), device) != cudaSuccess) return false;
+    void* dev = nullptr;
+    Mem m{};
+    if (by_pci(bus, &dev) != 0 || mem(dev, &m) != 0) return false;
+    *free_bytes = m.free;
+    *total_bytes = m.total;
+    return true;
+}
+
 // --------------------------------------------------------------- C-ABI
 extern "C" {
 
@@ -862,6 +898,31 @@ int gb_phase1_pmin(gb_dev* d, uint64_t a, uint64_t b, uint64_t* out, uint64_t n_
     return rc;
 }
 
+int gb_debug_tile(gb_dev* d, uint64_t a, uint64_t b, uint32_t block, uint32_t* out_words, int64_t* origin) {
+    if (!d || !out_words || !origin) GB_FAIL(d, GB_ERR_PARAM, "gb_debug_tile: null argument");
+    int rc = check_segment(d, a, b);
+    if (rc) return rc;
+    const uint64_t evens = ((b - a) >> 1) + 1;
+    if (evens > d->max_piece) GB_FAIL(d, GB_ERR_PARAM, "gb_debug_tile: segment larger than one piece");
+    if (block >= (evens + E6 - 1) / E6) GB_FAIL(d, GB_ERR_PARAM, "gb_debug_tile: no such block");
+    CU(d, cudaSetDevice(d->device));
+    uint32_t* d_tile = nullptr;
+    CU(d, dmalloc(d->device, &d_tile, 2 * M6W * 4));
+    Batch& s = d->sync;
+    s.pieces.assign(1, Piece{0, a, b});
+    rc = batch_launch(d, s, nullptr, d_tile, block);
+    if (rc == GB_OK) {
+        CU(d, cudaEventSynchronize(s.ev_done));
+        CU(d, cudaMemcpy(out_words, d_tile, 2 * M6W * 4, cudaMemcpyDeviceToHost));
+        const SegJob& j = s.h_jobs[0];
+        const int64_t q = j.qneg ? -(int64_t)j.qbase : (int64_t)j.qbase; // |Q| < 2^63 below the ceiling's reach
+        *origin = q + 6 * (int64_t)K6 * block;
+    }
+    s.launched = false;
+    dfree(d->device, d_tile);
+    return rc;
+}
+
 int gb_is_prime_batch(gb_dev* d, const uint64_t* values, uint8_t* out, uint64_t count) {
     if (!d) GB_FAIL(nullptr, GB_ERR_PARAM, "null handle");
     if (!count) return GB_OK;
@@ -932,6 +993,11 @@ int gb_device_memory(int device, uint64_t* free_bytes, uint64_t* total_bytes) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n)
         GB_FAIL(nullptr, GB_ERR_PARAM, "gb_device_memory: no such device");
+    // NVML first: it reads the device's memory without creating a CUDA
+    // context, so a resource check over every worker GPU (cli.cpp
+    // validate_resources) leaves the contexts to the worker threads, which
+    // create them in parallel
+    if (nvml_memory(device, free_bytes, total_bytes)) return GB_OK;
     int prev = 0;
     cudaGetDevice(&prev);
     cudaSetDevice(device);

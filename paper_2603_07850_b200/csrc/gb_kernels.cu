@@ -1507,6 +1507,13 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
             }
             const BlockInfo I = block_info(A, s_jobs, fb);
             sieve_block<ST>(A, tile, pat6, I, tid, BAR_S);
+            if (A.tile_out != nullptr && fb == A.tile_fb) { // parity hook (gb_debug_tile)
+                gbar<ST>(BAR_S);
+                for (uint32_t w = tid; w < M6W; w += ST) {
+                    A.tile_out[w] = arr_a(tile)[w];
+                    A.tile_out[M6W + w] = arr_b(tile)[w];
+                }
+            }
             nb_arrive(BAR_FULL + bs, NB);
         }
     } else {

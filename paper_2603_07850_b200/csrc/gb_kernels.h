@@ -47,6 +47,8 @@ struct VerifyArgs {
     unsigned int* list_count;
     uint32_t list_cap;
     uint64_t* pmin_out;           // optional per-even output (single slot)
+    uint32_t* tile_out;           // parity hook: the sieved tile of flat block tile_fb (A then B, 2 M6W words)
+    uint32_t tile_fb;
     // rows stop at iK0: tile primes from iK0 on are struck into qg by
     // k_mask_fill (iK0 = iB1 when the mask fill is off)
     uint32_t iK0;
