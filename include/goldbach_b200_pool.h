@@ -85,7 +85,14 @@ uint64_t gb_estimate_device_bytes(uint64_t cover_limit, uint64_t p_small,
 /* Message of the last failing pool / run call on this thread. */
 const char* gb_pool_last_error(void);
 
-/* Free / total memory of a device (cudaMemGetInfo). */
+/* Creates device's primary CUDA context (cudaSetDevice + cudaFree(0)).  The
+ * CLI calls it for every worker GPU on background threads while it checks
+ * resources, so context creation overlaps the check.  Not part of the
+ * reference interface. */
+int gb_warm_device(int device);
+
+/* Free / total memory of a device: NVML (no CUDA context needed), else
+ * cudaMemGetInfo. */
 int gb_device_memory(int device, uint64_t* free_bytes, uint64_t* total_bytes);
 
 #ifdef __cplusplus

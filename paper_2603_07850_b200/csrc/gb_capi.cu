@@ -989,6 +989,15 @@ uint64_t gb_estimate_device_bytes(uint64_t cover_limit, uint64_t p_small, uint64
     return np_all * (4 + 8) + (s / 16 + 64) + (uint64_t)(NBATCH + 1) * per_batch;
 }
 
+int gb_warm_device(int device) {
+    int n = 0;
+    if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n)
+        GB_FAIL(nullptr, GB_ERR_PARAM, "gb_warm_device: no such device");
+    if (cudaSetDevice(device) != cudaSuccess || cudaFree(nullptr) != cudaSuccess)
+        GB_FAIL(nullptr, GB_ERR_CUDA, "gb_warm_device: context creation failed");
+    return GB_OK;
+}
+
 int gb_device_memory(int device, uint64_t* free_bytes, uint64_t* total_bytes) {
     int n = 0;
     if (cudaGetDeviceCount(&n) != cudaSuccess || device < 0 || device >= n)

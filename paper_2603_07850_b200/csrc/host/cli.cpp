@@ -14,6 +14,8 @@
 #include <map>
 #include <ostream>
 #include <sstream>
+#include <thread>
+#include <vector>
 
 #include "goldbach/device.hpp"
 #include "goldbach/pool.hpp"
@@ -277,8 +279,24 @@ int run(const Config& cfg, std::ostream& out, std::ostream& err) {
     const bool dbg = getenv("GB_DEBUG_OPEN") != nullptr;
     const auto t_run = std::chrono::steady_clock::now();
     auto since = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t_run).count(); };
-    const MemoryEstimate est = validate_resources(cfg);
-    if (dbg) log.logf("timing: validate_resources ", since(), " s");
+    // the CUDA contexts of the worker GPUs are created in the background
+    // while the resources are checked (NVML, no context needed): on a cold
+    // process the context is the largest single cost before the first claim
+    std::vector<std::thread> warm;
+    {
+        const unsigned k = resolve_workers(cfg.workers);
+        const int g = std::max(1, visible_gpus());
+        for (unsigned i = 0; i < k && (int)i < g; ++i) warm.emplace_back([i] { gb_warm_device((int)i); });
+    }
+    MemoryEstimate est;
+    try {
+        est = validate_resources(cfg);
+    } catch (...) {
+        for (auto& t : warm) t.join();
+        throw;
+    }
+    for (auto& t : warm) t.join();
+    if (dbg) log.logf("timing: validate_resources + contexts ", since(), " s");
     log.logf("memory estimate: ", human_bytes(est.total_bytes), " (", est.workers, " GPU worker(s) x ",
              human_bytes(est.per_worker_bytes), " + shared ", human_bytes(est.shared_bytes), ")");
     // tables are built on each GPU by its worker (K1); the host keeps only
