@@ -76,7 +76,6 @@ struct Batch {
     std::vector<Piece> pieces;
     bool launched = false;
     bool timed = false;
-    bool large = false;
     bool pre = false;                   // pre-kernels timed (mask fill / large strike)
 };
 
@@ -239,7 +238,6 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out, uint32_t* tile_
         prefix += b.h_jobs[s].nblocks;
         max_qw = std::max(max_qw, b.h_jobs[s].qg_words);
     }
-    b.large = large;
     cudaStream_t st = d->serial ? d->sync.st : b.st;
     d->h2d_bytes += n * sizeof(SegJob);
     d->d2h_bytes += n * sizeof(DevRecord);

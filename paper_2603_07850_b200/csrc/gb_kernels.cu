@@ -581,7 +581,13 @@ __device__ __forceinline__ void strike_warp6(uint32_t* arr, uint32_t o, uint32_t
 // banks across the warp), where clearing a bit of a zero word is a no-op.
 static_assert(TPAD >= 32, "branch-free strikes need 32 pad words past each array");
 __device__ __forceinline__ void strike_if(uint32_t* arr, uint32_t c, uint32_t lane) {
-#if GB_PRED_STRIKE
+#if GB_PRED_STRIKE == 2
+    // predicated RED: a miss issues the instruction but moves no data
+    (void)lane;
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(arr) + ((c >> 3) & ~3u);
+    asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %0, %1;\n\t@p red.shared.and.b32 [%2], %3;\n\t}"
+                 ::"r"(c), "r"(M6), "r"(a), "r"(__funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, c)) : "memory");
+#elif GB_PRED_STRIKE
     strike(arr, min(c, M6 + 32 * lane));
 #else
     if (c < M6) strike(arr, c);
