@@ -423,6 +423,9 @@ def main():
                 "gbs": (traffic / avg_launch_s / 1e9) if traffic and avg_launch_s else None,
                 "peak_gbs": peaks.get("hbm_gbs"), "peak_source": "MEASURED_PEAKS.json hbm_gbs"},
         "ncu_profile": prof_w.get("source"),
+        # the kernel's own ceilings from that capture: the formula frac above
+        # counts reference-algorithm bytes; these are the pipes it actually fills
+        "ncu_pipes_pct": prof_w.get("pipes_pct"),
     }
 
     # ---- e2e through the public API, host <-> device copies included (one

@@ -140,6 +140,10 @@ def main():
         per_even = dram / a.evens_per_launch if a.evens_per_launch else None
         summ[key] = {"dram_bytes_per_launch_captured": dram, "evens_per_launch_captured": a.evens_per_launch,
                      "dram_bytes_per_even": per_even, "duration_ms_captured": dur * 1e3,
+                     "pipes_pct": {"issue_active": num("smsp__issue_active.avg.pct_of_peak_sustained_active"),
+                                   "alu": num("sm__inst_executed_pipe_alu.avg.pct_of_peak_sustained_active"),
+                                   "smem_wavefronts": num("l1tex__data_pipe_lsu_wavefronts_mem_shared.sum.pct_of_peak_sustained_elapsed"),
+                                   "l2_hit_rate": num("lts__t_sector_hit_rate.pct")},
                      "source": f"profiles/{a.tag}_ncu_verify.txt"}
         json.dump(summ, open(sp, "w"), indent=1)
     print("ok")
