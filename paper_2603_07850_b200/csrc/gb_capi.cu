@@ -65,6 +65,7 @@ struct Batch {
     SegJob* d_jobs = nullptr;
     uint4* d_pmc = nullptr;           // per slot {p, magic, c0} of the tile primes
     uint32_t* d_qg = nullptr;
+    uint32_t* d_k00 = nullptr;          // per-batch first indices of the primes > P_TILE_MAX (k_large_first)
     SlotAcc* d_acc = nullptr;
     StragEntry* d_list = nullptr;
     unsigned int* d_counters = nullptr; // [0] block counter, [1] list count
@@ -102,6 +103,7 @@ struct gb_dev {
     uint16_t* d_wsplit_heavy = nullptr; // the same for the heavy split
     uint16_t* d_wsplit_mask = nullptr;  // and for the mask split
     uint64_t* d_m64 = nullptr;          // floor(2^64 / p) per base prime
+    uint32_t* d_m32 = nullptr;          // floor(2^32 / p) per prime > P_TILE_MAX (GB_LS_PRE=0: none)
     uint64_t iL0 = 0, iL1 = 0;          // large primes
     // mask fill (k_mask_fill): tile primes [iK0, iB1) struck per 3-block
     // range into the large-prime bitmask instead of visited by every block
@@ -161,6 +163,7 @@ static int batch_alloc(gb_dev* d, Batch& b, bool with_qg) {
     CU(d, dmalloc(d->device, &b.d_pmc, (size_t)SLOTS * std::max<uint32_t>(np, 1) * sizeof(uint4)));
     if (with_qg && (d->iL1 > d->iL0 || d->mk_on))
         CU(d, dmalloc(d->device, &b.d_qg, (size_t)SLOTS * d->qg_stride * 4));
+    if (with_qg && d->d_m32) CU(d, dmalloc(d->device, &b.d_k00, (size_t)(d->iL1 - d->iL0) * 4));
     CU(d, dmalloc(d->device, &b.d_acc, SLOTS * sizeof(SlotAcc)));
     CU(d, dmalloc(d->device, &b.d_list, (size_t)LIST_CAP * sizeof(StragEntry)));
     CU(d, dmalloc(d->device, &b.d_counters, 4 * sizeof(unsigned int)));
@@ -180,6 +183,7 @@ static void batch_free(gb_dev* d, Batch& b) {
     dfree(d->device, b.d_jobs);
     dfree(d->device, b.d_pmc);
     dfree(d->device, b.d_qg);
+    dfree(d->device, b.d_k00);
     dfree(d->device, b.d_acc);
     dfree(d->device, b.d_list);
     dfree(d->device, b.d_counters);
@@ -270,8 +274,10 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out, uint32_t* tile_
         CU(d, cudaMemsetAsync(b.d_qg, 0xFF, (size_t)n * d->qg_stride * 4, st));
     }
     if (large) {
-        CU(d, launch_large_strike(b.d_jobs, n, d->d_primes, d->d_m64, d->iL0, d->iL1, b.d_qg, d->qg_stride, st));
-        d->launches++;
+        int nl = 0;
+        CU(d, launch_large_strike(b.d_jobs, n, d->d_primes, d->d_m64, d->iL0, d->iL1, b.d_qg, d->qg_stride, b.d_k00,
+                                  d->d_m32, &nl, st));
+        d->launches += nl;
     }
     VerifyArgs A{};
     A.jobs = b.d_jobs;
@@ -610,6 +616,11 @@ static int build_tables(gb_dev* d) {
     CU(d, dmalloc(d->device, &d->d_m64, std::max<uint64_t>(total, 1) * sizeof(uint64_t)));
     CU(d, launch_prime_magic64(d->d_primes, total, d->d_m64, d->sync.st));
     d->launches++;
+    if (d->iL1 > d->iL0 && !(getenv("GB_LS_PRE") && atoi(getenv("GB_LS_PRE")) == 0)) {
+        CU(d, dmalloc(d->device, &d->d_m32, (size_t)(d->iL1 - d->iL0) * 4));
+        CU(d, launch_large_m32(d->d_m64, d->iL0, d->iL1, d->d_m32, d->sync.st));
+        d->launches++;
+    }
     int rc2 = mask_plan(d, hp);
     if (rc2) return rc2;
     CU(d, cudaStreamSynchronize(d->sync.st)); // tables ready before any batch stream
@@ -756,6 +767,7 @@ int gb_close(gb_dev* d) {
     dfree(d->device, d->d_wsplit_heavy);
     dfree(d->device, d->d_wsplit_mask);
     dfree(d->device, d->d_m64);
+    dfree(d->device, d->d_m32);
     delete d;
     return GB_OK;
 }
@@ -981,10 +993,13 @@ uint64_t gb_estimate_device_bytes(uint64_t cover_limit, uint64_t p_small, uint64
     const uint64_t piece = std::min<uint64_t>(max_seg_evens, MAX_PIECE);
     // large-prime bitmask: primes > P_TILE_MAX, or the mask fill (s > M6)
     const uint64_t qg = s > M6 ? SLOTS * 2 * ((((piece + E6 - 1) / E6) * K6 + (M6 - K6) + 31) / 32) * 4 : 0;
-    const uint64_t per_batch = SLOTS * np_tile * sizeof(uint4) + qg + (uint64_t)LIST_CAP * (sizeof(StragEntry) + sizeof(StragResult)) +
+    // primes > P_TILE_MAX: per-batch first indices (k_large_first), 4 B each
+    const uint64_t np_large = np_all > np_tile ? np_all - np_tile : 0;
+    const uint64_t per_batch = SLOTS * np_tile * sizeof(uint4) + qg + np_large * 4 + (uint64_t)LIST_CAP * (sizeof(StragEntry) + sizeof(StragResult)) +
                                SLOTS * (sizeof(SegJob) + sizeof(SlotAcc) + sizeof(DevRecord)) + 64;
-    // base primes + their 64-bit magics + K1 scratch bitmap (transient) + NBATCH + 1 batches
-    return np_all * (4 + 8) + (s / 16 + 64) + (uint64_t)(NBATCH + 1) * per_batch;
+    // base primes + their 64-bit magics + the 32-bit magics of the large ones
+    // + K1 scratch bitmap (transient) + NBATCH + 1 batches
+    return np_all * (4 + 8) + np_large * 4 + (s / 16 + 64) + (uint64_t)(NBATCH + 1) * per_batch;
 }
 
 int gb_warm_device(int device) {

@@ -410,10 +410,40 @@ constexpr uint32_t LS_MAX_SLOTS = 16;
 // LS_GROUP slot bitmasks (16.7 MB each at 2e8-even segments) that stay in L2
 constexpr uint32_t LS_GROUP = GB_LS_GROUP;
 
+// 4 6^-1 mod p = 2 3^-1 mod p in closed form (p > 3 prime): (p + 2)/3 for
+// p = 1 (mod 3), (2p + 2)/3 for p = 2 (mod 3).  No loop, no 64-bit product.
+__device__ __forceinline__ uint32_t b_shift6_cf(uint32_t p) {
+    const uint32_t q3 = p / 3, r3 = p - 3 * q3;
+    return r3 == 1 ? q3 + 1 : 2 * q3 + 2;
+}
+
+// Once per batch: k00[i] = first index of array A at slot 0's window origin
+// for every prime above P_TILE_MAX (the 64-bit remainder), so that the
+// k_large_strike grid rows (one per LS_GROUP slots) derive their slots'
+// first indices with 32-bit arithmetic instead of each recomputing it.
+__global__ void __launch_bounds__(256) k_large_first(const SegJob* __restrict__ jobs,
+                                                     const uint32_t* __restrict__ primes,
+                                                     const uint64_t* __restrict__ m64, uint64_t iL0, uint64_t iL1,
+                                                     uint32_t* __restrict__ k00) {
+    const SegJob J = jobs[0];
+    for (uint64_t i = iL0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < iL1;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        k00[i - iL0] = first_a6(J, primes[i], m64[i]);
+}
+
+// m32[i] = floor(2^32 / p_i) = m64[i] >> 32, once per open
+__global__ void k_large_m32(const uint64_t* __restrict__ m64, uint64_t iL0, uint64_t iL1, uint32_t* __restrict__ m32) {
+    for (uint64_t i = iL0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < iL1;
+         i += (uint64_t)gridDim.x * blockDim.x)
+        m32[i - iL0] = (uint32_t)(m64[i] >> 32);
+}
+
 __global__ void __launch_bounds__(256) k_large_strike(const SegJob* __restrict__ jobs, uint32_t nslots,
                                                       const uint32_t* __restrict__ primes,
                                                       const uint64_t* __restrict__ m64, uint64_t iL0, uint64_t iL1,
-                                                      uint32_t* __restrict__ qg, uint64_t qg_stride_words) {
+                                                      uint32_t* __restrict__ qg, uint64_t qg_stride_words,
+                                                      const uint32_t* __restrict__ k00s,
+                                                      const uint32_t* __restrict__ m32s) {
     __shared__ SegJob s_jobs[LS_MAX_SLOTS];
     __shared__ uint32_t s_d[LS_MAX_SLOTS], s_near[LS_MAX_SLOTS];
     if (threadIdx.x < nslots) {
@@ -428,10 +458,16 @@ __global__ void __launch_bounds__(256) k_large_strike(const SegJob* __restrict__
     for (uint64_t i = iL0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < iL1;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t p = primes[i];
-        const uint64_t m = m64[i];
-        const uint32_t m32 = (uint32_t)(m >> 32); // <= floor(2^32 / p)
-        const uint32_t k00 = first_a6(s_jobs[0], p, m);
-        const uint32_t c = b_shift6(p);
+        uint32_t m32, k00;
+        if (k00s != nullptr) { // precomputed once per batch (k_large_first, k_large_m32)
+            m32 = m32s[i - iL0];
+            k00 = k00s[i - iL0];
+        } else {
+            const uint64_t m = m64[i];
+            m32 = (uint32_t)(m >> 32); // <= floor(2^32 / p)
+            k00 = first_a6(s_jobs[0], p, m);
+        }
+        const uint32_t c = b_shift6_cf(p);
         const uint32_t s1 = min(nslots, (blockIdx.y + 1) * LS_GROUP);
         for (uint32_t s = blockIdx.y * LS_GROUP; s < s1; ++s) {
             const SegJob& j = s_jobs[s];
@@ -442,7 +478,7 @@ __global__ void __launch_bounds__(256) k_large_strike(const SegJob* __restrict__
                 while (r >= p) r -= p;
                 k0 = k00 >= r ? k00 - r : k00 + (p - r);
             } else {
-                k0 = first_a6(j, p, m);
+                k0 = first_a6(j, p, m64[i]);
             }
             const uint32_t k0b = k0 >= c ? k0 - c : k0 + (p - c);
             const uint32_t ncells = j.qg_words * 32;
@@ -1779,13 +1815,24 @@ cudaError_t launch_segment_offsets(const SegJob* jobs, uint32_t nslots, const ui
     return cudaGetLastError();
 }
 cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, const uint64_t* m64,
-                                uint64_t iL0, uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, cudaStream_t st) {
+                                uint64_t iL0, uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, uint32_t* k00,
+                                const uint32_t* m32, int* nlaunch, cudaStream_t st) {
+    *nlaunch = 0;
     const uint64_t np = iL1 - iL0;
     if (!np || !nslots) return cudaSuccess;
     if (nslots > LS_MAX_SLOTS) return cudaErrorInvalidValue;
     const unsigned gx = (unsigned)std::min<uint64_t>((np + 255) / 256, 148ull * 16);
-    k_large_strike<<<dim3(gx, (nslots + LS_GROUP - 1) / LS_GROUP), 256, 0, st>>>(jobs, nslots, primes, m64, iL0,
-                                                                                 iL1, qg, qg_stride_words);
+    const bool pre = k00 != nullptr && m32 != nullptr && nslots > LS_GROUP; // one grid row: nothing to share
+    if (pre) k_large_first<<<gx, 256, 0, st>>>(jobs, primes, m64, iL0, iL1, k00);
+    *nlaunch = pre ? 2 : 1;
+    k_large_strike<<<dim3(gx, (nslots + LS_GROUP - 1) / LS_GROUP), 256, 0, st>>>(
+        jobs, nslots, primes, m64, iL0, iL1, qg, qg_stride_words, pre ? k00 : nullptr, pre ? m32 : nullptr);
+    return cudaGetLastError();
+}
+cudaError_t launch_large_m32(const uint64_t* m64, uint64_t iL0, uint64_t iL1, uint32_t* m32, cudaStream_t st) {
+    if (iL1 <= iL0) return cudaSuccess;
+    const unsigned gx = (unsigned)std::min<uint64_t>((iL1 - iL0 + 255) / 256, 148ull * 16);
+    k_large_m32<<<gx, 256, 0, st>>>(m64, iL0, iL1, m32);
     return cudaGetLastError();
 }
 cudaError_t launch_mask_fill(const MaskArgs& a, uint32_t max_qg_words, cudaStream_t st) {

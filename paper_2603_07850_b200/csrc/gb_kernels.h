@@ -87,7 +87,9 @@ cudaError_t launch_prime_magic64(const uint32_t* primes, uint64_t n, uint64_t* m
 cudaError_t launch_segment_offsets(const SegJob* jobs, uint32_t nslots, const uint32_t* primes,
                                    const uint64_t* m64, uint32_t iA0, uint32_t np, uint4* pmc, cudaStream_t st);
 cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, const uint64_t* m64,
-                                uint64_t iL0, uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, cudaStream_t st);
+                                uint64_t iL0, uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, uint32_t* k00,
+                                const uint32_t* m32, int* nlaunch, cudaStream_t st);
+cudaError_t launch_large_m32(const uint64_t* m64, uint64_t iL0, uint64_t iL1, uint32_t* m32, cudaStream_t st);
 cudaError_t launch_mask_fill(const MaskArgs& a, uint32_t max_qg_words, cudaStream_t st);
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st);
 cudaError_t launch_stragglers(const SegJob* jobs, const StragEntry* list, const unsigned int* list_count,
