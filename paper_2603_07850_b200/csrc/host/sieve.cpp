@@ -2,6 +2,8 @@
 // work is done by the sm_100a kernels; host code sizes buffers and copies.
 #include "goldbach/sieve.hpp"
 
+#include <algorithm>
+#include <bit>
 #include <cmath>
 #include <string>
 
@@ -52,12 +54,33 @@ std::vector<uint64_t> simple_sieve(uint64_t limit, uint64_t mem_cap_bytes) {
     if (need > mem_cap_bytes)
         throw ResourceError("simple_sieve: working set of " + std::to_string(need) + " bytes exceeds cap of " +
                             std::to_string(mem_cap_bytes) + " bytes");
-    if (limit > 0xFFFFFFFFull) throw ResourceError("simple_sieve: limit above 2^32 not supported on device");
-    std::vector<uint32_t> odd = device_odd_primes_upto(limit);
+    std::vector<uint32_t> odd = device_odd_primes_upto(std::min<uint64_t>(limit, 0xFFFFFFFFull));
     std::vector<uint64_t> out;
-    out.reserve(odd.size() + 1);
+    out.reserve(limit > 0xFFFFFFFFull ? (size_t)est : odd.size() + 1);
     out.push_back(2);
     for (uint32_t p : odd) out.push_back(p);
+    if (limit > 0xFFFFFFFFull) {
+        // above 2^32: the device segmented sieve (the fused kernels' K1
+        // interval kernel) in windows of 2^30 odd cells; the host only lists
+        // the set bits the reference API returns
+        auto sd = util_device(limit);
+        const uint64_t top = (limit & 1) ? limit : limit - 1; // largest odd <= limit
+        const uint64_t span = uint64_t{1} << 31; // integers per window
+        std::vector<uint64_t> w;
+        for (uint64_t lo = 0x100000001ull; lo <= top;) {
+            const uint64_t hi = top - lo >= span - 2 ? lo + span - 2 : top;
+            w.assign((((hi - lo) >> 1) + 1 + 63) / 64, 0);
+            sd->with([&](Device& d) {
+                d.check(gb_sieve_interval(d.get(), lo, hi, w.data(), w.size()));
+                return 0;
+            });
+            for (size_t k = 0; k < w.size(); ++k)
+                for (uint64_t b = w[k]; b; b &= b - 1)
+                    out.push_back(lo + 2 * ((uint64_t{k} << 6) + (uint64_t)std::countr_zero(b)));
+            if (hi == top) break;
+            lo = hi + 2;
+        }
+    }
     return out;
 }
 

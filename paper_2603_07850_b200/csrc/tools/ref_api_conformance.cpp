@@ -194,6 +194,10 @@ static void gpu_checks() {
     CHECK(rep.evens_checked == 4999 && rep.min_prime.p == 173 && rep.min_prime.n == 7426);
     const auto hit = phase2_resolve(18446744073709551614ull, small, p2);
     CHECK(hit && hit->p == 277);
+    // simple_sieve past 2^32 (the reference is bounded only by its memory cap,
+    // sieve.cpp:22-42): pi(2^32) = 203,280,221, then 56 primes to 2^32 + 1000
+    const std::vector<uint64_t> big = simple_sieve((uint64_t{1} << 32) + 1000);
+    CHECK(big.size() == 203'280'221ull + 56 && big[203'280'221] == 4294967311ull && big.back() == 4294968289ull);
     bool threw = false;
     try {
         const OddBitset small_q = tiled_sieve_segment(need.lo + 200, need.hi, build_base_primes(10'000));
