@@ -74,3 +74,20 @@ CASES = [
 def test_fused_tile_matches_oracle_sieve(gpu, cover, a, b, block, env):
     import oracle
     check_tile(gpu, oracle, cover, a, b, block, env)
+
+
+def test_fused_tiles_random_heights(gpu):
+    """Seeded random windows (the reference's seed 0xacce972) from 1e7 to
+    1e16: one piece of up to 2e8 evens, a random block of it, every cell."""
+    import random
+    import oracle
+    rng = random.Random(0xacce972)
+    for _ in range(8):
+        cover = int(10 ** rng.uniform(7, 16))
+        evens = rng.randint(1, 2 * 10**6)
+        a = rng.randrange(4, max(6, cover - 2 * evens), 2)
+        b = min(a + 2 * (evens - 1), cover - (cover & 1))
+        if b < a:
+            continue
+        nblocks = ((b - a) // 2 + 1 + 782303) // 782304
+        check_tile(gpu, oracle, cover, a, b, rng.randrange(nblocks))
