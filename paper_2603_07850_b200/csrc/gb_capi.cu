@@ -112,6 +112,7 @@ struct gb_dev {
     uint32_t iK0 = 0;
     uint32_t mk_p0 = 0;                 // smallest mask prime
     uint32_t force_sw = 0;              // GB_SW: force a compiled split (tuning)
+    bool pair = false;                  // GB_PAIR=1: k_verify_pair (2-CTA clusters share the single-strike rows)
     uint32_t* d_pat = nullptr;
     uint32_t* d_pat6 = nullptr;         // wheel-6 presieve patterns
     uint64_t* d_masks6 = nullptr;       // wheel-6 deep-window masks
@@ -236,10 +237,12 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out, uint32_t* tile_
     const bool large = d->iL1 > d->iL0;          // primes > P_TILE_MAX: k_large_strike
     const bool mask = d->mk_on && !d->mk_off_now; // tile primes >= iK0: k_mask_fill
     const bool use_qg = large || mask;
-    uint32_t prefix = 0, max_qw = 0;
+    uint32_t prefix = 0, max_qw = 0, pairs = 0;
     for (uint32_t s = 0; s < n; ++s) {
         make_job(d, b.pieces[s], b.h_jobs[s], prefix, use_qg);
+        b.h_jobs[s].pair_prefix = pairs;
         prefix += b.h_jobs[s].nblocks;
+        pairs += (b.h_jobs[s].nblocks + 1) / 2;
         max_qw = std::max(max_qw, b.h_jobs[s].qg_words);
     }
     cudaStream_t st = d->serial ? d->sync.st : b.st;
@@ -315,12 +318,15 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out, uint32_t* tile_
     A.list_count = b.d_counters + 1;
     A.list_cap = LIST_CAP;
     A.pmin_out = pmin_out;
+    A.total_pairs = pairs;
+    A.pair_counter = b.d_counters + 2;
     A.tile_out = tile_out;
     A.tile_fb = tile_fb;
     int grid = std::min<int>(d->sms * d->occ, (int)prefix);
     if (grid < 1) grid = 1;
     if (b.timed) CU(d, cudaEventRecord(b.ev_k0, st));
-    CU(d, launch_verify_blocks(A, grid, st));
+    if (d->pair) CU(d, launch_verify_pairs(A, grid, st));
+    else CU(d, launch_verify_blocks(A, grid, st));
     if (b.timed) CU(d, cudaEventRecord(b.ev_k1, st));
     CU(d, launch_stragglers(b.d_jobs, b.d_list, b.d_counters + 1, LIST_CAP, d->prm.p_small, b.d_res, pmin_out,
                             d->sms, st));
@@ -556,6 +562,8 @@ static int device_odd_primes_upto(gb_dev* d, uint64_t L, uint32_t** d_out, uint6
 static int mask_plan(gb_dev* d, const std::vector<uint32_t>& head) {
     d->mk_on = false;
     d->iK0 = d->iB1;
+    if (const char* e = getenv("GB_PAIR")) d->pair = atoi(e) != 0;
+    if (d->pair && pair_setup() != 0) GB_FAIL(d, GB_ERR_CUDA, "gb_open: cluster kernel attributes");
     if (const char* e = getenv("GB_SW")) {
         const uint32_t v = (uint32_t)atoi(e);
         if (v == WS_SW_LIGHT || v == WS_SW_HEAVY || v == WS_SW_MASK) d->force_sw = v;
@@ -733,6 +741,11 @@ int gb_open(int device, const gb_params* params, gb_dev** out) {
         d->qg_stride = 2 * ((blocks * K6 + (M6 - K6) + 31) / 32); // arrays A and B
         if ((rc = batch_alloc(d, d->sync, true)) != GB_OK) break;
         for (int i = 0; i < NBATCH && rc == GB_OK; ++i) rc = batch_alloc(d, d->batches[i], true);
+        if (getenv("GB_DEBUG_OPEN") && d->pair) {
+            int nc = 0;
+            pair_clusters_resident(&nc);
+            fprintf(stderr, "gb_open: pair mode, %d two-CTA clusters resident (of %d SMs)\n", nc, d->sms);
+        }
         if (getenv("GB_DEBUG_OPEN"))
             fprintf(stderr,
                     "gb_open: driver %.1f ms, context %.1f ms, kernels %.1f ms, setup %.1f ms, tables %.1f ms, "

@@ -151,6 +151,8 @@ struct SegJob {
     uint32_t qg_words;      // words per class array of the large-prime bitmask (0 = none)
     uint32_t delta;         // a - Q (in [PH6, PH6 + 5])
     uint32_t qmod[4];       // Q mod pg6_p(g) (non-negative)
+    uint32_t pair_prefix;   // flat index of this slot's first block pair (k_verify_pair)
+    uint32_t pad_;
 };
 
 // Per-slot accumulator written by the kernels.

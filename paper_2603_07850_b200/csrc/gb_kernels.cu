@@ -670,16 +670,112 @@ __device__ __forceinline__ void strike_rows(uint32_t* A6, uint32_t* B6, const ui
     for (; q < qe; q += GT) one(__ldg(q));
 }
 
+// ---- 2-CTA cluster pairing (k_verify_pair).  The CTAs of a cluster sieve
+// two consecutive blocks b0 = 2j, b0 + 1 of one slot.  A prime >= M6 (>= K6)
+// strikes each class array of a window at most once, and its offset in block
+// b0 + 1 follows from the one in b0 with one compare: o' = o - K6 (o >= K6)
+// or o + p - K6.  So each such row is visited ONCE per pair: the rows are
+// interleaved between the two CTAs, and every visit strikes its own tile
+// locally and the peer's tile through distributed shared memory.  mbarriers
+// (arrived remotely, release/acquire at cluster scope) order the peer's
+// presieve before the remote strikes, and the remote strikes before the
+// peer's check reads its tile.
+struct PairCtx {
+    uint32_t rank;        // 0: block b0, 1: block b0 + 1
+    bool own_valid;       // this CTA has a block in the pair (the last pair of an odd slot has one)
+    bool peer_valid;
+    uint32_t KB0;         // window start cell of b0
+    uint32_t peer_tile;   // shared::cluster address of the peer's tile (same buffer)
+    uint32_t peer_done;   // shared::cluster address of the peer's mb_done[buffer]
+};
+
+__device__ __forceinline__ uint32_t mapa_peer(uint32_t local_shared_addr, uint32_t peer) {
+    uint32_t r;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(r) : "r"(local_shared_addr), "r"(peer));
+    return r;
+}
+__device__ __forceinline__ void red_and_cluster(uint32_t addr, uint32_t v) {
+    asm volatile("red.shared::cluster.and.b32 [%0], %1;" ::"r"(addr), "r"(v) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_remote(uint32_t cluster_addr) {
+    asm volatile("mbarrier.arrive.release.cluster.shared::cluster.b64 _, [%0];" ::"r"(cluster_addr) : "memory");
+}
+// Wait for phase `parity` of a local mbarrier the peer arrives on; a
+// protocol error traps after ~2^32 cycles instead of hanging the GPU.
+__device__ __forceinline__ void mbar_wait_cluster(uint32_t addr, uint32_t parity) {
+    const long long t0 = clock64();
+    for (;;) {
+        uint32_t ok;
+        asm volatile("{\n\t.reg .pred p;\n\t"
+                     "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%1], %2;\n\t"
+                     "selp.u32 %0, 1, 0, p;\n\t}"
+                     : "=r"(ok) : "r"(addr), "r"(parity) : "memory");
+        if (ok) return;
+        if (clock64() - t0 > (1ll << 32)) __trap();
+    }
+}
+// The whole group waits for an mbarrier phase: one warp spins, the others
+// sleep at the group's named barrier (no issue slots taken from the check
+// warps), then every thread acquires the completed phase (returns at once).
+template <int GT>
+__device__ __forceinline__ void mbar_wait_group(uint32_t addr, uint32_t parity, uint32_t tid, int bar) {
+    if (tid < 32) mbar_wait_cluster(addr, parity);
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(GT) : "memory");
+    mbar_wait_cluster(addr, parity);
+}
+__device__ __forceinline__ void cluster_sync_all() {
+    asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+
+// Single-strike rows [q, qe) (stride GT2 = 2 GT, this CTA's interleave) for
+// both blocks of the pair: own block locally, the peer's through DSMEM.
+template <int GT2, int INF>
+__device__ __forceinline__ void strike_rows_pair(uint32_t* A6, uint32_t* B6, const uint4* q, const uint4* qe,
+                                                 const PairCtx& P, uint32_t lane) {
+    const uint32_t pa = P.peer_tile + 4 * TPAD, pb = P.peer_tile + 4 * (2 * TPAD + M6W);
+    auto one = [&](const uint4 v) {
+        uint32_t oa0, ob0;
+        block_off6(v, P.KB0, oa0, ob0);
+        const uint32_t p = v.x; // > K6
+        const uint32_t oa1 = oa0 >= K6 ? oa0 - K6 : oa0 + (p - K6);
+        const uint32_t ob1 = ob0 >= K6 ? ob0 - K6 : ob0 + (p - K6);
+        const uint32_t oa = P.rank ? oa1 : oa0, ob = P.rank ? ob1 : ob0; // own block
+        const uint32_t xa = P.rank ? oa0 : oa1, xb = P.rank ? ob0 : ob1; // peer's block
+        if (P.own_valid) {
+            strike_if(A6, oa, lane);
+            strike_if(B6, ob, lane);
+        }
+#ifndef GB_PAIR_NOREMOTE // timing probe: no remote strikes (wrong results)
+        if (P.peer_valid) {
+            if (xa < M6) red_and_cluster(pa + ((xa >> 3) & ~3u), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, xa));
+            if (xb < M6) red_and_cluster(pb + ((xb >> 3) & ~3u), __funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, xb));
+        }
+#else
+        (void)xa;
+        (void)xb;
+#endif
+    };
+    for (; q + (INF - 1) * GT2 < qe; q += INF * GT2) {
+        uint4 v[INF];
+#pragma unroll
+        for (int u = 0; u < INF; ++u) v[u] = __ldg(q + u * GT2);
+#pragma unroll
+        for (int u = 0; u < INF; ++u) one(v[u]);
+    }
+    for (; q < qe; q += GT2) one(__ldg(q));
+}
+
 // K2 strikes of one block by a group of GT threads (tid = index in the
 // group): warp-cooperative below P_WARP_MAX (rows wsplit[warp][..], balanced
 // by the host), one thread per prime above; primes >= M6 (index >= nW)
 // strike each array at most once.  pmc: this slot's rows (index i - iA0).
-template <int GT>
+template <int GT, bool PAIR = false>
 __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __restrict__ pmc, uint32_t nA,
                                                uint32_t nQ, uint32_t nH, uint32_t nW, uint32_t nB, uint32_t nK,
                                                uint32_t KB,
                                                uint32_t tid,
-                                               const uint16_t* __restrict__ wsplit) {
+                                               const uint16_t* __restrict__ wsplit, const PairCtx* P = nullptr,
+                                               uint32_t mb_ready = 0, uint32_t parity = 0, int bar = 0) {
     const uint32_t lane = tid & 31, warp = tid >> 5;
     uint32_t* A6 = arr_a(tile);
     uint32_t* B6 = arr_b(tile);
@@ -713,7 +809,16 @@ __device__ __forceinline__ void strike_verify6(uint32_t* tile, const uint4* __re
     constexpr int SS_INFLIGHT = GT == 32 * WS_SW_LIGHT ? GB_SS_INFLIGHT_LIGHT : GB_SS_INFLIGHT_HEAVY;
     strike_rows<GT, 2, SS_INFLIGHT>(A6, B6, pmc + nH + tid, pmc + nW, KB, lane);
 #ifndef GB_SKIP_SINGLE // timing probe: no single-strike primes (wrong results)
-    strike_rows<GT, 1, SS_INFLIGHT>(A6, B6, pmc + nW + tid, pmc + nB, KB, lane);
+    if constexpr (PAIR) {
+        // the peer has presieved its tile (remote strikes may start), then
+        // this CTA's interleave of the rows for both blocks
+        mbar_wait_group<GT>(mb_ready, parity, tid, bar);
+        strike_rows_pair<2 * GT, SS_INFLIGHT>(A6, B6, pmc + nW + P->rank * GT + tid, pmc + nB, *P, lane);
+    } else {
+        strike_rows<GT, 1, SS_INFLIGHT>(A6, B6, pmc + nW + tid, pmc + nB, KB, lane);
+    }
+#else
+    if constexpr (PAIR) mbar_wait_group<GT>(mb_ready, parity, tid, bar);
 #endif
 }
 
@@ -1270,9 +1375,28 @@ __device__ __forceinline__ BlockInfo block_info(const VerifyArgs& A, const SegJo
 // K2: sieve block I into tile by one group (tid = index in the group).  On
 // return this thread's strikes and fix-ups are issued; the caller's barrier
 // publishes them.
-template <int GT>
+template <int GT, bool PAIR = false>
 __device__ __forceinline__ void sieve_block(const VerifyArgs& A, uint32_t* tile, const uint32_t* pat6,
-                                            const BlockInfo& I, uint32_t tid, int bar) {
+                                            const BlockInfo& I, uint32_t tid, int bar, const PairCtx* P = nullptr,
+                                            uint32_t mb_ready = 0, uint32_t mb_done = 0, uint32_t peer_ready = 0,
+                                            uint32_t parity = 0) {
+    if constexpr (PAIR) {
+        if (!P->own_valid) {
+            // no block of our own in this pair (the last pair of a slot with
+            // an odd block count): our share of the peer's single-strike
+            // rows and the handshakes only
+            mbar_arrive_remote(peer_ready);
+            mbar_wait_group<GT>(mb_ready, parity, tid, bar);
+            const uint32_t nB = min(A.iB1, A.iK0) - A.iA0, nW = min(A.iW1 - A.iA0, nB);
+            const uint4* pmc = A.pmc + (size_t)I.s * A.np;
+            constexpr int SS_INFLIGHT = GT == 32 * WS_SW_LIGHT ? GB_SS_INFLIGHT_LIGHT : GB_SS_INFLIGHT_HEAVY;
+            strike_rows_pair<2 * GT, SS_INFLIGHT>(arr_a(tile), arr_b(tile), pmc + nW + P->rank * GT + tid, pmc + nB,
+                                                  *P, tid & 31);
+            mbar_arrive_remote(P->peer_done);
+            mbar_wait_group<GT>(mb_done, parity, tid, bar);
+            return;
+        }
+    }
     uint32_t pha[4], phb[4];
 #pragma unroll
     for (int g = 0; g < 4; ++g) {
@@ -1284,6 +1408,7 @@ __device__ __forceinline__ void sieve_block(const VerifyArgs& A, uint32_t* tile,
     presieve6(arr_a(tile), pat6, pha, tid, GT);
     presieve6(arr_b(tile), pat6, phb, tid, GT);
     gbar<GT>(bar);
+    if constexpr (PAIR) mbar_arrive_remote(peer_ready); // our presieve is visible: the peer may strike into us
     if (A.qg != nullptr && I.J.qg_words) {
         // large-prime mask words of this window (k_mask_fill, k_large_strike),
         // ANDed as REDs so they need no barrier against the strikes below
@@ -1313,10 +1438,18 @@ __device__ __forceinline__ void sieve_block(const VerifyArgs& A, uint32_t* tile,
         }
     }
 #ifndef GB_SKIP_STRIKES // timing probe: the check group on presieved-only tiles
-    strike_verify6<GT>(tile, A.pmc + (size_t)I.s * A.np, A.iA1 - A.iA0, A.iQ1 - A.iA0, A.iH1 - A.iA0,
-                       A.iW1 - A.iA0, A.iB1 - A.iA0, A.iK0 - A.iA0, I.KB, tid,
-                       A.wsplit);
+    strike_verify6<GT, PAIR>(tile, A.pmc + (size_t)I.s * A.np, A.iA1 - A.iA0, A.iQ1 - A.iA0, A.iH1 - A.iA0,
+                             A.iW1 - A.iA0, A.iB1 - A.iA0, A.iK0 - A.iA0, I.KB, tid,
+                             A.wsplit, P, mb_ready, parity, bar);
+#else
+    if constexpr (PAIR) mbar_wait_group<GT>(mb_ready, parity, tid, bar);
 #endif
+    if constexpr (PAIR) {
+        // our remote strikes into the peer are issued (release), and the
+        // peer's into us are complete before the fix-up and the check
+        mbar_arrive_remote(P->peer_done);
+        mbar_wait_group<GT>(mb_done, parity, tid, bar);
+    }
     if (I.low) {
         gbar<GT>(bar);
         fixup_low6(tile, I.Qs, A.primes, A.n_primes, A.sbound, tid, GT);
@@ -1573,6 +1706,127 @@ __global__ void __launch_bounds__(WS_THREADS, 1) k_verify_ws(VerifyArgs A) {
             nb_arrive(BAR_EMPTY + bs, NB);
         }
     }
+}
+
+// Paired variant of k_verify_ws: 2-CTA clusters, one block pair (b0, b0+1)
+// of a slot per cluster step, claimed by rank 0 and handed to rank 1 through
+// its shared memory.  Each CTA keeps the two-buffer sieve/check pipeline of
+// k_verify_ws; only the single-strike rows are shared (strike_rows_pair).
+// Flat block markers in s_fb: a block index, BLK_NONE (no block of ours in
+// this pair: the check group skips it) or BLK_END.
+constexpr uint32_t BLK_NONE = 0xFFFFFFFEu, BLK_END = 0xFFFFFFFFu;
+
+template <bool PMIN, int SW>
+__global__ void __launch_bounds__(WS_THREADS, 1) k_verify_pair(VerifyArgs A) {
+    constexpr int ST = 32 * SW, CT = WS_THREADS - ST;
+    extern __shared__ __align__(16) uint32_t smem[];
+    uint32_t* tiles = smem;
+    uint32_t* pat6 = smem + WS_PAT_OFF;
+    uint64_t* masks6 = (uint64_t*)(smem + WS_MASK_OFF);
+    __shared__ uint32_t s_fb[2];
+    __shared__ uint32_t s_pair[2];                   // claims from rank 0
+    __shared__ __align__(8) uint64_t mb_ready[2], mb_done[2], mb_claim[2];
+    __shared__ uint32_t s_q[CT / 32][QCAP];
+    __shared__ SegJob s_jobs[MAX_SLOTS];
+    uint32_t rank;
+    asm volatile("mov.u32 %0, %%cluster_ctarank;" : "=r"(rank));
+    const uint32_t peer = rank ^ 1u;
+
+    for (uint32_t i = threadIdx.x; i < PAT6_WORDS; i += blockDim.x) pat6[i] = A.gpat6[i];
+    for (uint32_t i = threadIdx.x; i < 3u * NWIN6; i += blockDim.x) masks6[i] = A.masks6[i];
+    for (uint32_t i = threadIdx.x; i < A.nslots * (uint32_t)(sizeof(SegJob) / 4); i += blockDim.x)
+        reinterpret_cast<uint32_t*>(s_jobs)[i] = reinterpret_cast<const uint32_t*>(A.jobs)[i];
+    for (uint32_t i = threadIdx.x; i < 2 * TILE6_WORDS; i += blockDim.x) tiles[i] = 0;
+    if (threadIdx.x == 0) {
+        for (int b = 0; b < 2; ++b) {
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&mb_ready[b])), "r"(ST));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&mb_done[b])), "r"(ST));
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(&mb_claim[b])), "r"(1));
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncthreads();
+    cluster_sync_all(); // both CTAs' barriers initialised before any remote arrive
+    const int NB = WS_THREADS;
+    if (threadIdx.x < ST) {
+        // ---- sieve group
+        const uint32_t tid = threadIdx.x;
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t bs = k & 1, parity = (k >> 1) & 1;
+            uint32_t* tile = tiles + bs * TILE6_WORDS;
+            if (k >= 2) nb_sync(BAR_EMPTY + bs, NB);
+            // claim pair k (rank 0) and hand it to rank 1
+            if (tid == 0) {
+                if (rank == 0) {
+                    const uint32_t pr = atomicAdd(A.pair_counter, 1u);
+                    s_pair[bs] = pr;
+                    const uint32_t rp = mapa_peer((uint32_t)__cvta_generic_to_shared(&s_pair[bs]), peer);
+                    asm volatile("st.shared::cluster.u32 [%0], %1;" ::"r"(rp), "r"(pr) : "memory");
+                    mbar_arrive_remote(mapa_peer((uint32_t)__cvta_generic_to_shared(&mb_claim[bs]), peer));
+                } else {
+                    mbar_wait_cluster((uint32_t)__cvta_generic_to_shared(&mb_claim[bs]), parity);
+                }
+                // pair -> own flat block
+                const uint32_t pr = s_pair[bs];
+                uint32_t fb = BLK_END;
+                if (pr < A.total_pairs) {
+                    uint32_t s = 0;
+                    while (s + 1 < A.nslots && s_jobs[s + 1].pair_prefix <= pr) ++s;
+                    const uint32_t b = 2 * (pr - s_jobs[s].pair_prefix) + rank;
+                    fb = b < s_jobs[s].nblocks ? s_jobs[s].block_prefix + b : BLK_NONE;
+                }
+                s_fb[bs] = fb;
+            }
+            gbar<ST>(BAR_S);
+            const uint32_t fb = s_fb[bs];
+            if (fb == BLK_END) {
+                if (k >= 1) nb_sync(BAR_EMPTY + (bs ^ 1), NB); // absorb the last EMPTY
+                nb_arrive(BAR_FULL + bs, NB);                  // check group sees the end
+                break;
+            }
+            // the pair's first block and whether each side has one
+            const uint32_t pr = s_pair[bs];
+            uint32_t s = 0;
+            while (s + 1 < A.nslots && s_jobs[s + 1].pair_prefix <= pr) ++s;
+            const uint32_t b0 = 2 * (pr - s_jobs[s].pair_prefix);
+            PairCtx P;
+            P.rank = rank;
+            P.own_valid = b0 + rank < s_jobs[s].nblocks;
+            P.peer_valid = b0 + peer < s_jobs[s].nblocks;
+            P.KB0 = b0 * K6;
+            P.peer_tile = mapa_peer((uint32_t)__cvta_generic_to_shared(tile), peer);
+            P.peer_done = mapa_peer((uint32_t)__cvta_generic_to_shared(&mb_done[bs]), peer);
+            const uint32_t peer_ready = mapa_peer((uint32_t)__cvta_generic_to_shared(&mb_ready[bs]), peer);
+            const BlockInfo I = block_info(A, s_jobs, s_jobs[s].block_prefix + b0 + (P.own_valid ? rank : 0));
+            sieve_block<ST, true>(A, tile, pat6, I, tid, BAR_S, &P, (uint32_t)__cvta_generic_to_shared(&mb_ready[bs]),
+                                  (uint32_t)__cvta_generic_to_shared(&mb_done[bs]), peer_ready, parity);
+            if (A.tile_out != nullptr && fb == A.tile_fb) {
+                gbar<ST>(BAR_S);
+                for (uint32_t w = tid; w < M6W; w += ST) {
+                    A.tile_out[w] = arr_a(tile)[w];
+                    A.tile_out[M6W + w] = arr_b(tile)[w];
+                }
+            }
+            nb_arrive(BAR_FULL + bs, NB);
+        }
+    } else {
+        // ---- check group
+        const uint32_t tid = threadIdx.x - ST;
+        for (uint32_t k = 0;; ++k) {
+            const uint32_t bs = k & 1;
+            nb_sync(BAR_FULL + bs, NB);
+            const uint32_t fb = s_fb[bs];
+            if (fb == BLK_END) break;
+            if (fb != BLK_NONE) {
+                const BlockInfo I = block_info(A, s_jobs, fb);
+#ifndef GB_SKIP_CHECK
+                check_block<PMIN, CT>(A, tiles + bs * TILE6_WORDS, masks6, I, tid, s_q);
+#endif
+            }
+            nb_arrive(BAR_EMPTY + bs, NB);
+        }
+    }
+    cluster_sync_all(); // no CTA leaves while its peer may still address its shared memory
 }
 
 // ============================================================ K4
@@ -1856,6 +2110,58 @@ cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st)
         else k_verify_ws<false, WS_SW_LIGHT><<<grid, WS_THREADS, WS_SMEM, st>>>(a);
     }
     return cudaGetLastError();
+}
+template <bool PMIN, int SW>
+static cudaError_t launch_pair_t(const VerifyArgs& a, int grid, cudaStream_t st) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)grid);
+    cfg.blockDim = dim3(WS_THREADS);
+    cfg.dynamicSmemBytes = WS_SMEM;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaLaunchKernelEx(&cfg, k_verify_pair<PMIN, SW>, a);
+}
+cudaError_t launch_verify_pairs(const VerifyArgs& a, int grid, cudaStream_t st) {
+    if (a.nslots > MAX_SLOTS) return cudaErrorInvalidValue;
+    grid &= ~1;
+    if (grid < 2) grid = 2;
+    cudaError_t e;
+    if (a.sw == WS_SW_HEAVY) e = a.pmin_out ? launch_pair_t<true, WS_SW_HEAVY>(a, grid, st) : launch_pair_t<false, WS_SW_HEAVY>(a, grid, st);
+    else if (a.sw == WS_SW_MASK) e = a.pmin_out ? launch_pair_t<true, WS_SW_MASK>(a, grid, st) : launch_pair_t<false, WS_SW_MASK>(a, grid, st);
+    else e = a.pmin_out ? launch_pair_t<true, WS_SW_LIGHT>(a, grid, st) : launch_pair_t<false, WS_SW_LIGHT>(a, grid, st);
+    if (e != cudaSuccess) return e;
+    return cudaGetLastError();
+}
+// per device, only when pair mode is used (lazy module loading keeps the
+// cluster kernels out of every other open)
+int pair_setup() {
+    return (cudaFuncSetAttribute(k_verify_pair<false, WS_SW_LIGHT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_SMEM) != cudaSuccess ||
+            cudaFuncSetAttribute(k_verify_pair<true, WS_SW_LIGHT>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_SMEM) != cudaSuccess ||
+            cudaFuncSetAttribute(k_verify_pair<false, WS_SW_HEAVY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_SMEM) != cudaSuccess ||
+            cudaFuncSetAttribute(k_verify_pair<true, WS_SW_HEAVY>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_SMEM) != cudaSuccess ||
+            cudaFuncSetAttribute(k_verify_pair<false, WS_SW_MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_SMEM) != cudaSuccess ||
+            cudaFuncSetAttribute(k_verify_pair<true, WS_SW_MASK>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)WS_SMEM) != cudaSuccess)
+               ? 1 : 0;
+}
+int pair_clusters_resident(int* clusters) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(296);
+    cfg.blockDim = dim3(WS_THREADS);
+    cfg.dynamicSmemBytes = WS_SMEM;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 2;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cudaOccupancyMaxActiveClusters(clusters, k_verify_pair<false, WS_SW_HEAVY>, &cfg) == cudaSuccess ? 0 : 1;
 }
 cudaError_t launch_stragglers(const SegJob* jobs, const StragEntry* list, const unsigned int* list_count,
                               uint32_t list_cap, uint64_t p_small, StragResult* res, uint64_t* pmin_out,

@@ -49,6 +49,8 @@ struct VerifyArgs {
     uint64_t* pmin_out;           // optional per-even output (single slot)
     uint32_t* tile_out;           // parity hook: the sieved tile of flat block tile_fb (A then B, 2 M6W words)
     uint32_t tile_fb;
+    uint32_t total_pairs;         // k_verify_pair: block pairs of the batch (2-CTA clusters)
+    unsigned int* pair_counter;
     // rows stop at iK0: tile primes from iK0 on are struck into qg by
     // k_mask_fill (iK0 = iB1 when the mask fill is off)
     uint32_t iK0;
@@ -92,6 +94,11 @@ cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint3
 cudaError_t launch_large_m32(const uint64_t* m64, uint64_t iL0, uint64_t iL1, uint32_t* m32, cudaStream_t st);
 cudaError_t launch_mask_fill(const MaskArgs& a, uint32_t max_qg_words, cudaStream_t st);
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st);
+// paired variant: 2-CTA clusters, each single-strike row visited once per
+// block pair (grid rounded down to whole clusters)
+cudaError_t launch_verify_pairs(const VerifyArgs& a, int grid, cudaStream_t st);
+int pair_clusters_resident(int* clusters);
+int pair_setup(); // cluster kernels' shared-memory attribute (pair mode only)
 cudaError_t launch_stragglers(const SegJob* jobs, const StragEntry* list, const unsigned int* list_count,
                               uint32_t list_cap, uint64_t p_small, StragResult* res, uint64_t* pmin_out,
                               int grid, cudaStream_t st);

@@ -93,3 +93,21 @@ def test_reference_api_conformance_gpu(gpu):
     out = subprocess.run([exe, "--gpu"], capture_output=True, text=True, timeout=300)
     assert out.returncode == 0, out.stdout + out.stderr[-2000:]
     assert "conformance ok" in out.stdout
+
+
+@pytest.mark.parametrize("cover,a,n", CASES + [(10**12, 10**12 - 2 * 3_000_000 + 2, 3_000_000)])
+def test_pair_mode_equals_default(gpu, cover, a, n):
+    """k_verify_pair (2-CTA clusters sharing the single-strike rows through
+    DSMEM, GB_PAIR=1) against the default kernel; the last case has an odd
+    block count (4 blocks + a partial one) so one CTA of the last pair has
+    no block of its own."""
+    b = a + 2 * (n - 1)
+    with _open(gpu, cover) as dev:
+        want = _rec(dev, a, b)
+    os.environ["GB_PAIR"] = "1"
+    try:
+        dev = _open(gpu, cover)
+    finally:
+        del os.environ["GB_PAIR"]
+    with dev:
+        assert _rec(dev, a, b) == want
