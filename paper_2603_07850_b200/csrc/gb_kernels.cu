@@ -446,6 +446,9 @@ __global__ void __launch_bounds__(256) k_large_strike(const SegJob* __restrict__
                                                       const uint32_t* __restrict__ m32s) {
     __shared__ SegJob s_jobs[LS_MAX_SLOTS];
     __shared__ uint32_t s_d[LS_MAX_SLOTS], s_near[LS_MAX_SLOTS];
+    __shared__ uint32_t s_dmax; // largest d of this grid row's slots (all near) or ~0
+    if (threadIdx.x == 0) s_dmax = 0;
+    __syncthreads();
     if (threadIdx.x < nslots) {
         const SegJob j = jobs[threadIdx.x], j0 = jobs[0];
         s_jobs[threadIdx.x] = j;
@@ -453,14 +456,19 @@ __global__ void __launch_bounds__(256) k_large_strike(const SegJob* __restrict__
         const bool near = !j.qneg && !j0.qneg && j.qbase >= j0.qbase && (j.qbase - j0.qbase) / 6 < (1ull << 32);
         s_near[threadIdx.x] = near;
         s_d[threadIdx.x] = near ? (uint32_t)((j.qbase - j0.qbase) / 6) : 0;
+        if (threadIdx.x >= blockIdx.y * LS_GROUP && threadIdx.x < (blockIdx.y + 1) * LS_GROUP)
+            atomicMax(&s_dmax, near ? s_d[threadIdx.x] : 0xFFFFFFFFu);
     }
     __syncthreads();
+    const uint32_t dmax = s_dmax;
     for (uint64_t i = iL0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < iL1;
          i += (uint64_t)gridDim.x * blockDim.x) {
         const uint32_t p = primes[i];
         uint32_t m32, k00;
         if (k00s != nullptr) { // precomputed once per batch (k_large_first, k_large_m32)
-            m32 = m32s[i - iL0];
+            // primes above every slot offset of this row need no remainder
+            // of d (d mod p = d), so their 32-bit magic is not even loaded
+            m32 = p > dmax ? 0u : m32s[i - iL0];
             k00 = k00s[i - iL0];
         } else {
             const uint64_t m = m64[i];
@@ -474,8 +482,11 @@ __global__ void __launch_bounds__(256) k_large_strike(const SegJob* __restrict__
             uint32_t k0;
             if (s_near[s]) {
                 const uint32_t d = s_d[s];
-                uint32_t r = d - __umulhi(d, m32) * p; // d mod p, quotient low by <= 2
-                while (r >= p) r -= p;
+                uint32_t r = d;
+                if (d >= p) { // d mod p, quotient low by <= 2
+                    r = d - __umulhi(d, m32) * p;
+                    while (r >= p) r -= p;
+                }
                 k0 = k00 >= r ? k00 - r : k00 + (p - r);
             } else {
                 k0 = first_a6(j, p, m64[i]);
