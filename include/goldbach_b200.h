@@ -164,14 +164,15 @@ int gb_is_prime_batch(gb_dev* dev, const uint64_t* values, uint8_t* out,
 
 /* Parity hook for the fused kernel's own sieve (K2): runs [a, b] (one piece)
  * and copies the wheel-6 tile of block `block` right after its sieve, before
- * the check reads it: out_words[0 .. 8191] = array A (bit k of word w <->
- * q = origin + 6 (32 w + k)), out_words[8192 .. 16383] = array B (q = origin
- * + 4 + 6 (32 w + k)); *origin = the block's window origin Q_b (1 mod 6,
- * negative near the start of the number line).  Bit set <=> q prime, for
- * every q <= the handle's cover limit.  Not part of the reference interface;
- * below 2^63 only. */
+ * the check reads it.  *words_per_array = W (the tile's words per class
+ * array; out_words == NULL only queries it).  out_words[0 .. W-1] = array A
+ * (bit k of word w <-> q = origin + 6 (32 w + k)), out_words[W .. 2W-1] =
+ * array B (q = origin + 4 + 6 (32 w + k)), cap_words >= 2W; *origin = the
+ * block's window origin Q_b (1 mod 6, negative near the start of the number
+ * line).  Bit set <=> q prime, for every q <= the handle's cover limit.  Not
+ * part of the reference interface; below 2^63 only. */
 int gb_debug_tile(gb_dev* dev, uint64_t a, uint64_t b, uint32_t block, uint32_t* out_words,
-                  int64_t* origin);
+                  uint64_t cap_words, uint32_t* words_per_array, int64_t* origin);
 
 /* Device Phase 2 resolver (phase2_resolve, verifier.cpp:129-165) for one
  * even n >= 4 with the handle's p_small: *p = minimal prime p (0 when none,

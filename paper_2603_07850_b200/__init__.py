@@ -150,7 +150,8 @@ def lib():
         "gb_kernel_times": ([vp, C.POINTER(C.c_double), p64, i32], i32),
         "gb_set_timing": ([vp, i32], i32),
         "gb_set_bucket": ([vp, i32], i32),
-        "gb_debug_tile": ([vp, u64, u64, C.c_uint32, C.POINTER(C.c_uint32), C.POINTER(C.c_int64)], i32),
+        "gb_debug_tile": ([vp, u64, u64, C.c_uint32, C.POINTER(C.c_uint32), u64, C.POINTER(C.c_uint32),
+                           C.POINTER(C.c_int64)], i32),
         "gb_bucket_info": ([vp, p64], i32),
         "gb_io_bytes": ([vp, p64, p64], i32),
         "gb_flush_l2": ([vp], i32),
@@ -323,16 +324,24 @@ class Device:
         """0/False off, 1/True event timing, 2 timing with serialised batches."""
         _check(lib().gb_set_timing(self._h, int(mode)), self._h)
 
+    def tile_words(self) -> int:
+        """Words per class array of the fused kernel's wheel-6 tile."""
+        nw = C.c_uint32()
+        _check(lib().gb_debug_tile(self._h, 0, 0, 0, None, 0, C.byref(nw), None), self._h)
+        return nw.value
+
     def debug_tile(self, a: int, b: int, block: int):
         """The fused kernel's sieved wheel-6 tile of one block (parity hook):
         (origin Q, A words, B words); A bit k <-> q = Q + 6k, B bit k <->
         q = Q + 4 + 6k."""
         import numpy as np
-        w = np.zeros(2 * 8192, dtype=np.uint32)
+        nw = C.c_uint32()
         q = C.c_int64()
-        _check(lib().gb_debug_tile(self._h, a, b, block, w.ctypes.data_as(C.POINTER(C.c_uint32)),
-                                   C.byref(q)), self._h)
-        return q.value, w[:8192], w[8192:]
+        n = self.tile_words()
+        w = np.zeros(2 * n, dtype=np.uint32)
+        _check(lib().gb_debug_tile(self._h, a, b, block, w.ctypes.data_as(C.POINTER(C.c_uint32)), 2 * n,
+                                   C.byref(nw), C.byref(q)), self._h)
+        return q.value, w[:n], w[n:]
 
     def set_bucket(self, enabled: bool):
         """Mask fill of the large tile primes on/off (results are identical)."""

@@ -921,8 +921,12 @@ int gb_phase1_pmin(gb_dev* d, uint64_t a, uint64_t b, uint64_t* out, uint64_t n_
     return rc;
 }
 
-int gb_debug_tile(gb_dev* d, uint64_t a, uint64_t b, uint32_t block, uint32_t* out_words, int64_t* origin) {
-    if (!d || !out_words || !origin) GB_FAIL(d, GB_ERR_PARAM, "gb_debug_tile: null argument");
+int gb_debug_tile(gb_dev* d, uint64_t a, uint64_t b, uint32_t block, uint32_t* out_words, uint64_t cap_words,
+                  uint32_t* words_per_array, int64_t* origin) {
+    if (!d || !words_per_array) GB_FAIL(d, GB_ERR_PARAM, "gb_debug_tile: null argument");
+    *words_per_array = M6W;
+    if (!out_words) return GB_OK; // size query
+    if (!origin || cap_words < 2ull * M6W) GB_FAIL(d, GB_ERR_PARAM, "gb_debug_tile: output too small");
     int rc = check_segment(d, a, b);
     if (rc) return rc;
     const uint64_t evens = ((b - a) >> 1) + 1;

@@ -75,26 +75,36 @@ constexpr int N_PAT_PRIMES = 14;
 // The fused kernel sieves a wheel-6 tile: array A holds q = Q + 6k
 // (q = 1 mod 6), array B holds q = Q + 4 + 6k (q = 5 mod 6), k < M6; Q = 1
 // (mod 6) is the block's window origin.  Multiples of 2 and 3 have no cell,
-// so a 64 KiB tile spans 6 M6 = 1.57 M integers (odd-only: 1.05 M) and an
+// so an 80 KiB tile spans 6 M6 = 1.97 M integers (odd-only: 1.31 M) and an
 // even n meets only the candidates p with n - p = +-1 (mod 6).  Blocks of a
 // slot advance by K6 cells (a multiple of 32, so global bitmask words align)
 // and hold E6 = 3 K6 evens; consecutive windows overlap by 6 (M6 - K6) > PH6
 // integers, the Phase 1 halo.
-constexpr uint32_t M6 = 1u << 18;             // cells per class array
+#ifndef GB_M6
+// cells per class array (a multiple of 32): 1.25 x 2^18 measured best (1e13
+// 4.53 s against 4.68 s at 2^18, C5 0.165 against 0.167 s, 1e12 equal);
+// 1.375 x 2^18 no longer fits two tile buffers in shared memory
+#define GB_M6 327680
+#endif
+constexpr uint32_t M6 = GB_M6;                // cells per class array
 constexpr uint32_t M6W = M6 / 32;             // words per class array
-constexpr uint32_t K6 = 260768;               // block stride in cells (32 * 8149)
-constexpr uint32_t E6 = 3 * K6;               // evens per block (782304)
+constexpr uint32_t K6 = M6 - 1376;            // block stride in cells (a multiple of 32: 326304 = 32 * 10197)
+constexpr uint32_t E6 = 3 * K6;               // evens per block (978912)
 constexpr uint32_t PH6 = 8193;                // in-tile candidates p <= PH6
 constexpr int NWIN6 = 22;                     // 64-wide g-windows, g = p div 6 <= 1365
 constexpr uint32_t TPAD = 32;                 // zero words before / after each array (misses of branch-free strikes land here)
 constexpr uint32_t TILE6_WORDS = 3 * TPAD + 2 * M6W; // [pad][A][pad][B][pad]
-static_assert(K6 % 32 == 0 && 6 * (M6 - K6) > PH6 + 5, "wheel-6 block geometry");
+static_assert(M6 % 32 == 0 && K6 % 32 == 0 && 6 * (M6 - K6) > PH6 + 5, "wheel-6 block geometry");
+// deep-even queue entries: t (class index in the block, < K6 + 32) | ci | window j
+constexpr int DQ_CI = K6 + 32 <= (1u << 18) ? 18 : 19;
+constexpr int DQ_J = DQ_CI + 2;
+static_assert(K6 + 32 <= (1u << DQ_CI) && DQ_J + 5 <= 32, "deep queue entry layout");
 static_assert(64 * NWIN6 * 6 >= PH6, "deep windows cover the halo");
 
 // ------------------------------------------------------------- mask fill
 // k_mask_fill: one CTA per MK_CELLS cells (3 block strides) of both class
 // arrays of a slot's large-prime bitmask, held in shared memory.
-constexpr uint32_t MK_CELLS = 3 * K6;               // 782304 (a multiple of 32)
+constexpr uint32_t MK_CELLS = (M6 <= 262144 ? 3 : 2) * K6; // the most of 3 / 2 strides that fits (a multiple of 32)
 constexpr uint32_t MK_WORDS = MK_CELLS / 32;        // per array
 constexpr uint32_t MK_THREADS = 512;
 constexpr size_t MK_SMEM = 2ull * MK_WORDS * 4;     // 195.6 KB: one CTA per SM

@@ -1020,7 +1020,7 @@ __device__ __forceinline__ void deep_even6(const uint32_t* tile, const uint64_t*
 }
 
 // One round over the warp's deep-even queue: the top n entries
-// (t | ci << 18 | j << 20) each test ONE window j; misses are pushed back
+// (t | ci << DQ_CI | j << DQ_J) each test ONE window j; misses are pushed back
 // with j + 1, so no lane idles while another walks many windows.
 template <bool PMIN>
 __device__ __forceinline__ uint32_t deep_round6(const uint32_t* tile, const uint64_t* masks6, uint32_t* q, uint32_t qn,
@@ -1034,7 +1034,7 @@ __device__ __forceinline__ uint32_t deep_round6(const uint32_t* tile, const uint
     if (lane == 0) GB_STAT(3, 1);
     bool again = false;
     if (act) {
-        const uint32_t t = e & 0x3FFFFu, ci = (e >> 18) & 3u, j = e >> 20;
+        const uint32_t t = e & ((1u << DQ_CI) - 1), ci = (e >> DQ_CI) & 3u, j = e >> DQ_J;
         const Class6 C = CL[ci];
         const uint32_t p = window_hit6(tile, masks6, C.r, C.G, t, j, ~0ull, ~0ull, ~0ull);
         const uint32_t il = ci + 3 * t;
@@ -1049,7 +1049,7 @@ __device__ __forceinline__ uint32_t deep_round6(const uint32_t* tile, const uint
         }
     }
     const uint32_t bal = __ballot_sync(0xffffffffu, again);
-    if (again) q[qn + __popc(bal & ((1u << lane) - 1))] = e + (1u << 20);
+    if (again) q[qn + __popc(bal & ((1u << lane) - 1))] = e + (1u << DQ_J);
     __syncwarp();
     return qn + __popc(bal);
 }
@@ -1320,7 +1320,7 @@ __device__ __forceinline__ uint32_t word_deep(const uint32_t* tile, const uint64
     if (qn + total <= QCAP) {
         uint32_t pos = qn + pre;
         const uint32_t t0 = 32 * w - delta; // wraps for w = 0; t0 + bit >= 0 for valid bits
-        const uint32_t hi = (ci << 18) | (deep_j0(C.r) << 20);
+        const uint32_t hi = (ci << DQ_CI) | (deep_j0(C.r) << DQ_J);
         while (U) {
             const uint32_t bit = __ffs(U) - 1;
             U &= U - 1;

@@ -15,8 +15,6 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-M6 = 1 << 18
-
 
 def expand(words):
     """bit k of the class array (LSB-first u32 words) as a bool array"""
@@ -35,7 +33,11 @@ def check_tile(gb, oracle, cover, a, b, block, env=None):
             else:
                 os.environ[k] = v
     with dev:
+        if block < 0:  # counted from the last block of the piece
+            e6 = 3 * (32 * dev.tile_words() - 1376)
+            block += ((b - a) // 2 + 1 + e6 - 1) // e6
         Q, A, B = dev.debug_tile(a, b, block)
+    M6 = 32 * len(A)  # cells per class array of this build
     assert Q % 6 == 1
     top = min(cover, b)
     lo = max(Q, 3) | 1
@@ -63,7 +65,7 @@ CASES = [
     (10**8, 4, 10**8, 0, None),                                        # low window: q <= 1, base primes restored
     (10**8, 4, 10**8, 1, None),
     (10**12, 10**12 - 400_000_000 + 2, 10**12, 0, None),             # C3 rows
-    (10**12, 10**12 - 400_000_000 + 2, 10**12, 255, None),           # last block of a segment
+    (10**12, 10**12 - 400_000_000 + 2, 10**12, -1, None),            # last block of a segment
     (10**13, 10**13 - 400_000_000 + 2, 10**13, 117, None),           # C4 heavy split
     (10**13, 10**13 - 400_000_000 + 2, 10**13, 117, {"GB_MASK_P": "262145"}),  # mask fill
     (4 * 10**18 + 10**11, 4 * 10**18, 4 * 10**18 + 400_000_000 - 2, 3, None),  # k_large_strike bitmask
@@ -89,5 +91,7 @@ def test_fused_tiles_random_heights(gpu):
         b = min(a + 2 * (evens - 1), cover - (cover & 1))
         if b < a:
             continue
-        nblocks = ((b - a) // 2 + 1 + 782303) // 782304
+        with gpu.Device(cover) as d0:
+            e6 = 3 * (32 * d0.tile_words() - 1376)  # evens per block
+        nblocks = ((b - a) // 2 + 1 + e6 - 1) // e6
         check_tile(gpu, oracle, cover, a, b, rng.randrange(nblocks))
