@@ -75,21 +75,23 @@ constexpr int N_PAT_PRIMES = 14;
 // The fused kernel sieves a wheel-6 tile: array A holds q = Q + 6k
 // (q = 1 mod 6), array B holds q = Q + 4 + 6k (q = 5 mod 6), k < M6; Q = 1
 // (mod 6) is the block's window origin.  Multiples of 2 and 3 have no cell,
-// so an 80 KiB tile spans 6 M6 = 1.97 M integers (odd-only: 1.31 M) and an
+// so a 96 KiB tile spans 6 M6 = 2.36 M integers (odd-only: 1.57 M) and an
 // even n meets only the candidates p with n - p = +-1 (mod 6).  Blocks of a
 // slot advance by K6 cells (a multiple of 32, so global bitmask words align)
 // and hold E6 = 3 K6 evens; consecutive windows overlap by 6 (M6 - K6) > PH6
 // integers, the Phase 1 halo.
 #ifndef GB_M6
-// cells per class array (a multiple of 32): 1.25 x 2^18 measured best (1e13
-// 4.53 s against 4.68 s at 2^18, C5 0.165 against 0.167 s, 1e12 equal);
-// 1.375 x 2^18 no longer fits two tile buffers in shared memory
-#define GB_M6 327680
+// cells per class array (a multiple of 32).  Larger tiles visit each row prime
+// per more cells: 2^18 / 1.25 / 1.375 / 1.5 x 2^18 measured 1e12 0.366 /
+// 0.366 / 0.363 / 0.358 s and 1e13 4.68 / 4.52 / 4.46 / 4.35 s (same
+// checksums); 1.5 x 2^18 is the largest that fits two tile buffers beside
+// 128-entry deep queues (GB_QCAP)
+#define GB_M6 393216
 #endif
 constexpr uint32_t M6 = GB_M6;                // cells per class array
 constexpr uint32_t M6W = M6 / 32;             // words per class array
-constexpr uint32_t K6 = M6 - 1376;            // block stride in cells (a multiple of 32: 326304 = 32 * 10197)
-constexpr uint32_t E6 = 3 * K6;               // evens per block (978912)
+constexpr uint32_t K6 = M6 - 1376;            // block stride in cells (a multiple of 32: 391840 = 32 * 12245)
+constexpr uint32_t E6 = 3 * K6;               // evens per block (1175520)
 constexpr uint32_t PH6 = 8193;                // in-tile candidates p <= PH6
 constexpr int NWIN6 = 22;                     // 64-wide g-windows, g = p div 6 <= 1365
 constexpr uint32_t TPAD = 32;                 // zero words before / after each array (misses of branch-free strikes land here)

@@ -950,7 +950,10 @@ constexpr uint32_t DEEP_J0_R0 = ((BS6_PMAX_R0 + 1) / 6) / 64;
 constexpr uint32_t DEEP_J0_R24 = ((BS6_PMAX_R24 + 1) / 6) / 64;
 __device__ __forceinline__ uint32_t deep_j0(uint32_t r) { return r == 0 ? DEEP_J0_R0 : DEEP_J0_R24; }
 constexpr int NPL = BS6_PLANES;          // z planes
-constexpr uint32_t QCAP = 512;           // per-warp deep-even queue (classes 2, 4 run ~2x the mean deep rate)
+#ifndef GB_QCAP
+#define GB_QCAP 128 // 512 before the 1.5 x 2^18 tile (equal speed at 256 / 128)
+#endif
+constexpr uint32_t QCAP = GB_QCAP;       // per-warp deep-even queue (classes 2, 4 run ~2x the mean deep rate)
 
 // Straggler entry for an even with no candidate inside the in-tile halo.
 __device__ __forceinline__ void push_straggler(const VerifyArgs& A, const SegJob& J, uint32_t s, uint32_t iseg,
