@@ -38,7 +38,10 @@ constexpr int THREADS = 512;            // threads per CTA of k_sieve_interval
 #endif
 constexpr int WS_THREADS = GB_WS_THREADS;
 constexpr int WS_SW_LIGHT = GB_WS_SW_LIGHT, WS_SW_HEAVY = GB_WS_SW_HEAVY, WS_SW_MASK = GB_WS_SW_MASK;
-constexpr uint32_t WS_HEAVY_PRIMES = 150000;
+// row primes above which the heavy split is taken: beyond every tile (at
+// most pi(2^22) rows) since the 1.5 x 2^18 tile (1e13: 12 sieve warps 4.23 s,
+// 16 warps 4.35 s; it was 16 below 2^18-cell tiles); GB_SW=16 still selects it
+constexpr uint32_t WS_HEAVY_PRIMES = 400000;
 constexpr uint32_t WS_MASK_PRIMES = 50000; // row primes at or below: the mask split
 // warps of the group that runs the warp-cooperative strikes (max of the splits)
 constexpr int SPLIT_WARPS = WS_SW_HEAVY > WS_SW_LIGHT ? WS_SW_HEAVY : WS_SW_LIGHT;
