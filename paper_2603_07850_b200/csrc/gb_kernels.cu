@@ -1121,7 +1121,7 @@ __device__ __forceinline__ uint32_t idx_sum(uint32_t x) {
 // words per vertical-counter reduction: longer batches amortise the flush
 // but widen the counters (registers); the check group's size decides
 #ifndef GB_VFLUSH_LIGHT
-#define GB_VFLUSH_LIGHT 16 // 16 check warps: 16 steps per class, one flush
+#define GB_VFLUSH_LIGHT 24 // 16 check warps: 24 steps per class with the 1.5 x 2^18 tile, one flush
 #endif
 #ifndef GB_VFLUSH_HEAVY
 #define GB_VFLUSH_HEAVY 22 // 12 check warps: 22 steps per class, one flush
