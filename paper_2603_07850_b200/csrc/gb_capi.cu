@@ -105,6 +105,9 @@ struct gb_dev {
     uint64_t* d_m64 = nullptr;          // floor(2^64 / p) per base prime
     uint32_t* d_m32 = nullptr;          // floor(2^32 / p) per prime > P_TILE_MAX (GB_LS_PRE=0: none)
     uint64_t iL0 = 0, iL1 = 0;          // large primes
+    uint64_t iLB = 0;                   // first large prime of the batch walk (k_large_batch); iL1 = none
+    uint32_t ls_cop = 0;                // k_large_rows skips multiples of 5..13 (1) and 17..23 (2) (GB_LS_COP; default 0: measured slower)
+    bool ls_rows = true;                // row walk (k_large_rows) for batches on one axis (GB_LS_ROWS=0: per slot)
     // mask fill (k_mask_fill): tile primes [iK0, iB1) struck per 3-block
     // range into the large-prime bitmask instead of visited by every block
     bool mk_on = false;                 // plan built
@@ -231,6 +234,40 @@ static void make_job(gb_dev* d, const Piece& pc, SegJob& j, uint32_t prefix, boo
     j.qg_words = use_qg ? (uint32_t)(((uint64_t)j.nblocks * K6 + (M6 - K6) + 31) / 32) : 0;
 }
 
+// Slot table of k_large_batch: every slot on slot 0's wheel axis (origin
+// Q_0, q = Q_0 + 6k), ascending, the span below 2^32 cells, and each window
+// overlapping at most its neighbours' (the halo), so that a cell lies in the
+// last slot starting at or below it or in the one before.
+static bool large_batch_tab(const SegJob* J, uint32_t n, LargeBatchTab& T) {
+    if (n == 0 || n > MAX_SLOTS) return false;
+    for (uint32_t s = 0; s < MAX_SLOTS; ++s) T.d[s] = ~0u;
+    uint64_t span = 0;
+    for (uint32_t s = 0; s < n; ++s) {
+        if (J[s].qneg || J[s].qbase < J[0].qbase) return false;
+        const uint64_t dd = (J[s].qbase - J[0].qbase) / 6;
+        const uint64_t end = dd + (uint64_t)J[s].qg_words * 32;
+        if (end >= (1ull << 32) - 1) return false;
+        if (s > 0 && dd < T.d[s - 1]) return false;
+        if (s > 1 && dd < (uint64_t)T.d[s - 2] + (uint64_t)J[s - 2].qg_words * 32) return false;
+        T.d[s] = (uint32_t)dd;
+        T.qw[s] = J[s].qg_words;
+        T.qm[s][0] = (uint32_t)(J[s].qbase % 5005);
+        T.qm[s][1] = (uint32_t)((J[s].qbase % 5005 + 4) % 5005);
+        T.qm2[s][0] = (uint32_t)(J[s].qbase % 7429);
+        T.qm2[s][1] = (uint32_t)((J[s].qbase % 7429 + 4) % 7429);
+        span = std::max(span, end);
+    }
+    // k_large_rows forms 6 o + (origin mod 7429) for o below a row's span
+    for (uint32_t s = 0; s < n; s += 2) {
+        const uint64_t e0 = (uint64_t)J[s].qg_words * 32;
+        const uint64_t e1 = s + 1 < n ? (uint64_t)(T.d[s + 1] - T.d[s]) + (uint64_t)J[s + 1].qg_words * 32 : 0;
+        if (6 * std::max(e0, e1) + 7429 >= (1ull << 32)) return false;
+    }
+    T.n = n;
+    T.span = (uint32_t)span;
+    return true;
+}
+
 static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out, uint32_t* tile_out = nullptr,
                         uint32_t tile_fb = 0) {
     const uint32_t n = (uint32_t)b.pieces.size();
@@ -277,10 +314,21 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out, uint32_t* tile_
         CU(d, cudaMemsetAsync(b.d_qg, 0xFF, (size_t)n * d->qg_stride * 4, st));
     }
     if (large) {
+        // sparse primes walk the batch once when its slots line up on one
+        // wheel axis (consecutive claims); otherwise every large prime takes
+        // the per-row path
+        LargeBatchTab T{};
+        const bool axis = large_batch_tab(b.h_jobs, n, T);
+        T.cop = d->ls_cop;
+        const uint64_t iLB = axis && d->iLB < d->iL1 ? d->iLB : d->iL1;
         int nl = 0;
-        CU(d, launch_large_strike(b.d_jobs, n, d->d_primes, d->d_m64, d->iL0, d->iL1, b.d_qg, d->qg_stride, b.d_k00,
-                                  d->d_m32, &nl, st));
+        CU(d, launch_large_strike(b.d_jobs, n, d->d_primes, d->d_m64, d->iL0, iLB, b.d_qg, d->qg_stride, b.d_k00,
+                                  d->d_m32, axis && d->ls_rows ? &T : nullptr, &nl, st));
         d->launches += nl;
+        if (iLB < d->iL1) {
+            CU(d, launch_large_batch(b.d_jobs, T, d->d_primes, d->d_m64, iLB, d->iL1, b.d_qg, d->qg_stride, st));
+            d->launches++;
+        }
     }
     VerifyArgs A{};
     A.jobs = b.d_jobs;
@@ -628,6 +676,27 @@ static int build_tables(gb_dev* d) {
         CU(d, dmalloc(d->device, &d->d_m32, (size_t)(d->iL1 - d->iL0) * 4));
         CU(d, launch_large_m32(d->d_m64, d->iL0, d->iL1, d->d_m32, d->sync.st));
         d->launches++;
+    }
+    // batch-walk threshold (k_large_batch): large primes from GB_LB_T
+    // (default 0 = off: measured slower) by a binary search
+    // of the device table
+    d->iLB = d->iL1;
+    if (d->iL1 > d->iL0) {
+        uint64_t t = 0;
+        if (const char* e = getenv("GB_LB_T")) t = strtoull(e, nullptr, 0);
+        if (const char* e = getenv("GB_LS_ROWS")) d->ls_rows = atoi(e) != 0;
+        if (const char* e = getenv("GB_LS_COP")) d->ls_cop = (uint32_t)atoi(e);
+        if (t != 0) {
+            uint64_t lo = d->iL0, hi = d->iL1; // first index with p >= t
+            while (lo < hi) {
+                const uint64_t mid = lo + (hi - lo) / 2;
+                uint32_t v = 0;
+                CU(d, cudaMemcpy(&v, d->d_primes + mid, 4, cudaMemcpyDeviceToHost));
+                if (v < t) lo = mid + 1;
+                else hi = mid;
+            }
+            d->iLB = lo;
+        }
     }
     int rc2 = mask_plan(d, hp);
     if (rc2) return rc2;

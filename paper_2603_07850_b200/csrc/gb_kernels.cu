@@ -511,6 +511,167 @@ __global__ void __launch_bounds__(256) k_large_strike(const SegJob* __restrict__
     }
 }
 
+// Primes at or above the batch threshold (sparse primes: a few multiples per
+// batch at most): one visit per prime and batch instead of one per grid row
+// of k_large_strike.  The batch's slots are ascending and near (host-checked,
+// LargeBatchTab), so every slot window is the range [d_s, d_s + nc_s) of one
+// coordinate axis k (q = Q_0 + 6k) that starts at slot 0's origin.  The
+// thread walks the prime's multiples k0, k0 + p, ... below the span end once
+// per class array, finds the last slot with d_s <= k by a predicated scan of
+// the register-resident origins, and strikes that slot and, in the halo
+// overlap, the one before it (the reference's sparse-prime hit list,
+// sieve.cpp:109-126, made a batch-wide walk).  No per-slot remainders, no
+// per-slot loops: ~1/8 of k_large_strike's work for these primes.
+__device__ __forceinline__ void lb_strike_walk(uint32_t k, uint32_t p, const LargeBatchTab& T,
+                                               const uint32_t* __restrict__ s_d, const uint32_t* __restrict__ s_nc, const uint32_t* __restrict__ s_base,
+                                               uint32_t* __restrict__ qg) {
+    while (k < T.span) {
+        uint32_t s = 0;
+#pragma unroll
+        for (uint32_t j = 1; j < MAX_SLOTS; ++j) s += k >= T.d[j]; // unused slots: d = ~0
+        const uint32_t o = k - s_d[s];
+        if (o < s_nc[s]) atomicAnd(qg + s_base[s] + (o >> 5), ~(1u << (o & 31)));
+        if (s > 0) { // halo overlap with the previous slot's window
+            const uint32_t o1 = k - s_d[s - 1];
+            if (o1 < s_nc[s - 1]) atomicAnd(qg + s_base[s - 1] + (o1 >> 5), ~(1u << (o1 & 31)));
+        }
+        if (p >= T.span - k) break; // no 32-bit wrap near the 2^64 ceiling
+        k += p;
+    }
+}
+
+__global__ void __launch_bounds__(256) k_large_batch(const SegJob* __restrict__ jobs, LargeBatchTab T,
+                                                     const uint32_t* __restrict__ primes,
+                                                     const uint64_t* __restrict__ m64, uint64_t i0, uint64_t i1,
+                                                     uint32_t* __restrict__ qg, uint64_t qg_stride_words) {
+    // per slot: cells per class array, word offsets of arrays A and B
+    __shared__ uint32_t s_d[MAX_SLOTS], s_nc[MAX_SLOTS], s_ba[MAX_SLOTS], s_bb[MAX_SLOTS];
+    __shared__ SegJob s_j0;
+    if (threadIdx.x < MAX_SLOTS) {
+        const uint32_t s = threadIdx.x;
+        s_d[s] = T.d[s];
+        const uint32_t qw = s < T.n ? jobs[s].qg_words : 0;
+        s_nc[s] = qw * 32;
+        s_ba[s] = (uint32_t)(s * qg_stride_words);
+        s_bb[s] = (uint32_t)(s * qg_stride_words) + qw;
+    }
+    if (threadIdx.x == 0) s_j0 = jobs[0];
+    __syncthreads();
+    for (uint64_t i = i0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < i1;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = primes[i];
+        const uint32_t k0 = first_a6(s_j0, p, m64[i]);
+        const uint32_t c = b_shift6_cf(p);
+        const uint32_t k0b = k0 >= c ? k0 - c : k0 + (p - c);
+        lb_strike_walk(k0, p, T, s_d, s_nc, s_ba, qg);
+        lb_strike_walk(k0b, p, T, s_d, s_nc, s_bb, qg);
+    }
+}
+
+// k_large_strike's grid rows when the batch's slots line up on one wheel axis
+// (LargeBatchTab, host-checked): a row of LS_GROUP slots is one range
+// [D, E) of that axis, so a prime takes ONE remainder for the row (the first
+// multiple at or above D, from its batch first index k00) and walks its
+// multiples through the range, striking each slot of the row whose window
+// holds the cell (both, in the halo overlap).  Against the per-slot form
+// this drops the per-slot remainders, folds and loop set-ups.  Rows run in
+// grid order, so the REDs of one row stay in the row's L2-resident masks.
+// FIRST: the launch of row 0 (D = 0), which computes each prime's batch
+// first index k00 itself (64-bit, first_a6 at slot 0's origin) and stores it
+// for the launch of the other rows (no separate k_large_first pass).  The
+// prime tables stream through L2 with evict-first loads, so the row's slot
+// masks stay resident for the REDs.
+template <bool FIRST>
+__global__ void __launch_bounds__(256) k_large_rows(LargeBatchTab T, const SegJob* __restrict__ jobs,
+                                                    const uint32_t* __restrict__ primes,
+                                                    const uint64_t* __restrict__ m64, uint64_t iL0, uint64_t iL1,
+                                                    uint32_t* __restrict__ qg, uint64_t qg_stride_words,
+                                                    uint32_t* __restrict__ k00s,
+                                                    const uint32_t* __restrict__ m32s, uint32_t row0) {
+    static_assert(LS_GROUP == 2, "row walk written for two slots per row");
+    // T.cop >= 1, s_cop bit x (x < 5005): gcd(x, 5*7*11*13) = 1.  A multiple q
+    // of a large prime that 5, 7, 11 or 13 also divides is already clear in
+    // the tile (the presieve), so its RED can be skipped: 42 % of the strikes
+    // for two remainders per strike.  Off by default: the row walk is
+    // issue-bound (72 % issue active), and the remainders cost more than the
+    // REDs they save (C5 window 0.140 s off, 0.163 s at 1, 0.196 s at 2).
+    __shared__ uint32_t s_cop[(5005 + 31) / 32];
+    if (T.cop && threadIdx.x < (5005 + 31) / 32) {
+        const uint32_t w = threadIdx.x * 32;
+        // bit b of P_p set iff b mod p != 0 (b < 64); word = P_p >> (w mod p)
+        constexpr uint64_t P5 = 0xEF7BDEF7BDEF7BDEull, P7 = 0x7EFDFBF7EFDFBF7Eull;
+        constexpr uint64_t P11 = 0xFF7FEFFDFFBFF7FEull, P13 = 0xFFEFFF7FFBFFDFFEull;
+        s_cop[threadIdx.x] = (uint32_t)(P5 >> (w % 5)) & (uint32_t)(P7 >> (w % 7)) & (uint32_t)(P11 >> (w % 11)) &
+                             (uint32_t)(P13 >> (w % 13));
+    }
+    // s_cop2 bit x (x < 7429): gcd(x, 17*19*23) = 1 (T.cop >= 2: a further
+    // 15 % of the remaining strikes for one more remainder per strike)
+    __shared__ uint32_t s_cop2[(7429 + 31) / 32];
+    if (T.cop >= 2 && threadIdx.x < (7429 + 31) / 32) {
+        const uint32_t w = threadIdx.x * 32;
+        constexpr uint64_t P17 = 0xFFF7FFFBFFFDFFFEull, P19 = 0xFDFFFFBFFFF7FFFEull, P23 = 0xFFFFBFFFFF7FFFFEull;
+        s_cop2[threadIdx.x] = (uint32_t)(P17 >> (w % 17)) & (uint32_t)(P19 >> (w % 19)) &
+                              (uint32_t)(P23 >> (w % 23));
+    }
+    __shared__ SegJob s_j0;
+    if (FIRST && threadIdx.x == 0) s_j0 = jobs[0];
+    __syncthreads();
+    const uint32_t s0 = (row0 + blockIdx.y) * LS_GROUP;
+    const bool two = s0 + 1 < T.n;
+    const uint32_t D = T.d[s0];
+    const uint32_t nc0 = T.qw[s0] * 32;
+    const uint32_t dl = two ? T.d[s0 + 1] - D : 0;  // second slot's start within the row
+    const uint32_t nc1 = two ? T.qw[s0 + 1] * 32 : 0;
+    const uint32_t L = max(nc0, dl + nc1);          // row range [D, D + L)
+    uint32_t* const a0 = qg + s0 * qg_stride_words; // slot s0: A, then B at + qgw
+    uint32_t* const b0 = a0 + T.qw[s0];
+    uint32_t* const a1 = a0 + qg_stride_words;
+    uint32_t* const b1 = two ? a1 + T.qw[s0 + 1] : a1;
+    for (uint64_t i = iL0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < iL1;
+         i += (uint64_t)gridDim.x * blockDim.x) {
+        const uint32_t p = __ldcs(primes + i);
+        uint32_t k00, r = D; // r = D mod p (quotient of the 32-bit magic low by <= 2)
+        if (FIRST) {
+            k00 = first_a6(s_j0, p, __ldcs(m64 + i));
+            __stcs(k00s + (i - iL0), k00);
+        } else {
+            k00 = __ldcs(k00s + (i - iL0));
+            if (D >= p) {
+                r = D - __umulhi(D, __ldcs(m32s + (i - iL0))) * p;
+                while (r >= p) r -= p;
+            }
+        }
+        const uint32_t oa = k00 >= r ? k00 - r : k00 + (p - r);
+        const uint32_t c = b_shift6_cf(p);
+        const uint32_t ob = oa >= c ? oa - c : oa + (p - c);
+#pragma unroll
+        for (int arr = 0; arr < 2; ++arr) {
+            uint32_t* const w0 = arr ? b0 : a0;
+            uint32_t* const w1 = arr ? b1 : a1;
+            const uint32_t q0 = T.qm[s0][arr], q1 = T.qm[s0 + two][arr]; // slot origin (+4 for B) mod 5005
+            const uint32_t r0 = T.qm2[s0][arr], r1 = T.qm2[s0 + two][arr]; // ... mod 7429
+            for (uint32_t o = arr ? ob : oa; o < L;) {
+                const uint32_t o1 = o - dl; // wraps above nc1 when o < dl
+                bool h0 = o < nc0, h1 = o1 < nc1;
+                if (T.cop) {
+                    const uint32_t x = (q0 + 6 * o) % 5005u, x1 = (q1 + 6 * o1) % 5005u;
+                    h0 = h0 && (s_cop[x >> 5] >> (x & 31) & 1);
+                    h1 = h1 && (s_cop[x1 >> 5] >> (x1 & 31) & 1);
+                    if (T.cop >= 2) {
+                        const uint32_t y = (r0 + 6 * o) % 7429u, y1 = (r1 + 6 * o1) % 7429u;
+                        h0 = h0 && (s_cop2[y >> 5] >> (y & 31) & 1);
+                        h1 = h1 && (s_cop2[y1 >> 5] >> (y1 & 31) & 1);
+                    }
+                }
+                if (h0) atomicAnd(w0 + (o >> 5), ~(1u << (o & 31)));
+                if (h1) atomicAnd(w1 + (o1 >> 5), ~(1u << (o1 & 31)));
+                if (p >= L - o) break; // 32-bit steps cannot wrap
+                o += p;
+            }
+        }
+    }
+}
+
 // Window cells of the first strikes of {p, m, z, c'} in arrays A and B of
 // the block starting at cell KB: z = k0 + p ceil(2^29 / p) (so z - KB >= 0
 // for every block start), A's offset is (z - KB) mod p by the magic
@@ -2084,17 +2245,35 @@ cudaError_t launch_segment_offsets(const SegJob* jobs, uint32_t nslots, const ui
 }
 cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, const uint64_t* m64,
                                 uint64_t iL0, uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, uint32_t* k00,
-                                const uint32_t* m32, int* nlaunch, cudaStream_t st) {
+                                const uint32_t* m32, const LargeBatchTab* T, int* nlaunch, cudaStream_t st) {
     *nlaunch = 0;
     const uint64_t np = iL1 - iL0;
     if (!np || !nslots) return cudaSuccess;
     if (nslots > LS_MAX_SLOTS) return cudaErrorInvalidValue;
     const unsigned gx = (unsigned)std::min<uint64_t>((np + 255) / 256, 148ull * 16);
+    if (T != nullptr && k00 != nullptr && m32 != nullptr) { // slots on one axis: the row walk
+        const unsigned rows = (nslots + LS_GROUP - 1) / LS_GROUP;
+        k_large_rows<true><<<dim3(gx, 1), 256, 0, st>>>(*T, jobs, primes, m64, iL0, iL1, qg, qg_stride_words, k00, m32, 0);
+        *nlaunch = 1;
+        if (rows > 1) {
+            k_large_rows<false><<<dim3(gx, rows - 1), 256, 0, st>>>(*T, jobs, primes, m64, iL0, iL1, qg, qg_stride_words,
+                                                                    k00, m32, 1);
+            *nlaunch = 2;
+        }
+        return cudaGetLastError();
+    }
     const bool pre = k00 != nullptr && m32 != nullptr && nslots > LS_GROUP; // one grid row: nothing to share
     if (pre) k_large_first<<<gx, 256, 0, st>>>(jobs, primes, m64, iL0, iL1, k00);
     *nlaunch = pre ? 2 : 1;
     k_large_strike<<<dim3(gx, (nslots + LS_GROUP - 1) / LS_GROUP), 256, 0, st>>>(
         jobs, nslots, primes, m64, iL0, iL1, qg, qg_stride_words, pre ? k00 : nullptr, pre ? m32 : nullptr);
+    return cudaGetLastError();
+}
+cudaError_t launch_large_batch(const SegJob* jobs, const LargeBatchTab& T, const uint32_t* primes, const uint64_t* m64,
+                               uint64_t i0, uint64_t i1, uint32_t* qg, uint64_t qg_stride_words, cudaStream_t st) {
+    if (i1 <= i0 || !T.n) return cudaSuccess;
+    const unsigned gx = (unsigned)std::min<uint64_t>((i1 - i0 + 255) / 256, 148ull * 16);
+    k_large_batch<<<gx, 256, 0, st>>>(jobs, T, primes, m64, i0, i1, qg, qg_stride_words);
     return cudaGetLastError();
 }
 cudaError_t launch_large_m32(const uint64_t* m64, uint64_t iL0, uint64_t iL1, uint32_t* m32, cudaStream_t st) {

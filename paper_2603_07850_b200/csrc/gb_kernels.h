@@ -56,6 +56,20 @@ struct VerifyArgs {
     uint32_t iK0;
 };
 
+// Slot layout of one batch on a common wheel axis (k_large_batch): slot s's
+// window is cells [d[s], d[s] + its qg_words * 32) of q = Q_0 + 6k.  Valid only
+// for ascending, near slots whose windows overlap at most their neighbours
+// (host-checked per batch); unused entries d = ~0.
+struct LargeBatchTab {
+    uint32_t d[MAX_SLOTS];
+    uint32_t qw[MAX_SLOTS]; // qg_words of each slot
+    uint32_t qm[MAX_SLOTS][2]; // (slot origin + 4 arr) mod 5005, arr 0 = A, 1 = B
+    uint32_t qm2[MAX_SLOTS][2]; // the same mod 7429
+    uint32_t cop;  // k_large_rows: skip strikes of multiples of 5, 7, 11, 13 (1), and of 17, 19, 23 (2); 0 = none
+    uint32_t n;    // slots
+    uint32_t span; // max over s of d[s] + cells of slot s
+};
+
 struct MaskArgs {
     const SegJob* jobs;           // qg_words per slot
     uint32_t nslots;
@@ -90,7 +104,9 @@ cudaError_t launch_segment_offsets(const SegJob* jobs, uint32_t nslots, const ui
                                    const uint64_t* m64, uint32_t iA0, uint32_t np, uint4* pmc, cudaStream_t st);
 cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, const uint64_t* m64,
                                 uint64_t iL0, uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, uint32_t* k00,
-                                const uint32_t* m32, int* nlaunch, cudaStream_t st);
+                                const uint32_t* m32, const LargeBatchTab* T, int* nlaunch, cudaStream_t st);
+cudaError_t launch_large_batch(const SegJob* jobs, const LargeBatchTab& T, const uint32_t* primes, const uint64_t* m64,
+                               uint64_t i0, uint64_t i1, uint32_t* qg, uint64_t qg_stride_words, cudaStream_t st);
 cudaError_t launch_large_m32(const uint64_t* m64, uint64_t iL0, uint64_t iL1, uint32_t* m32, cudaStream_t st);
 cudaError_t launch_mask_fill(const MaskArgs& a, uint32_t max_qg_words, cudaStream_t st);
 cudaError_t launch_verify_blocks(const VerifyArgs& a, int grid, cudaStream_t st);
