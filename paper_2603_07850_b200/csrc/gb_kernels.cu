@@ -28,7 +28,8 @@ namespace gbk {
 #ifdef GB_STATS
 // debug counters (variant builds only): 0 generic evens, 1 in-place deep
 // evens (queue overflow), 2 queued deep evens, 3 deep rounds, 4 stragglers,
-// 5 fast blocks, 6 generic blocks
+// 5 fast blocks, 6 generic blocks, 7 large-prime REDs outside their slot's
+// bitmask (GB_LS_BOUNDS builds: counted and dropped; must stay 0)
 __device__ unsigned long long g_stats[8];
 #define GB_STAT(i, v) atomicAdd(&g_stats[i], (unsigned long long)(v))
 #else
@@ -663,6 +664,14 @@ __global__ void __launch_bounds__(256) k_large_rows(LargeBatchTab T, const SegJo
                         h1 = h1 && (s_cop2[y1 >> 5] >> (y1 & 31) & 1);
                     }
                 }
+#ifdef GB_LS_BOUNDS // bounds probe (compute-sanitizer is unavailable on the GPU pool)
+                auto inside = [&](const uint32_t* w) {
+                    const uint64_t off = (uint64_t)(w - qg), s = off / qg_stride_words;
+                    return s < T.n && off - s * qg_stride_words < 2ull * T.qw[s];
+                };
+                if (h0 && !inside(w0 + (o >> 5))) { GB_STAT(7, 1); h0 = false; }
+                if (h1 && !inside(w1 + (o1 >> 5))) { GB_STAT(7, 1); h1 = false; }
+#endif
                 if (h0) atomicAnd(w0 + (o >> 5), ~(1u << (o & 31)));
                 if (h1) atomicAnd(w1 + (o1 >> 5), ~(1u << (o1 & 31)));
                 if (p >= L - o) break; // 32-bit steps cannot wrap
