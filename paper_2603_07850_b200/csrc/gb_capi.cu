@@ -74,6 +74,7 @@ struct Batch {
     SegJob* h_jobs = nullptr;
     DevRecord* h_rec = nullptr;
     cudaEvent_t ev_done = nullptr, ev_k0 = nullptr, ev_k1 = nullptr, ev_l0 = nullptr, ev_s1 = nullptr;
+    cudaEvent_t ev_first = nullptr;     // after the large-prime launches (k00 written; gb_dev::chain_b)
     std::vector<Piece> pieces;
     bool launched = false;
     bool timed = false;
@@ -107,6 +108,9 @@ struct gb_dev {
     uint64_t iL0 = 0, iL1 = 0;          // large primes
     uint64_t iLB = 0;                   // first large prime of the batch walk (k_large_batch); iL1 = none
     uint32_t ls_cop = 0;                // k_large_rows skips multiples of 5..13 (1) and 17..23 (2) (GB_LS_COP; default 0: measured slower)
+    Batch* chain_b = nullptr;           // batch whose k00 buffer holds the last row walk's first indices
+    uint64_t chain_q0 = 0;              // ... and its slot-0 origin (|Q|, positive)
+    bool ls_chain = true;               // derive k00 from chain_b's (GB_LS_CHAIN=0: 64-bit remainder per batch)
     bool ls_rows = true;                // row walk (k_large_rows) for batches on one axis (GB_LS_ROWS=0: per slot)
     // mask fill (k_mask_fill): tile primes [iK0, iB1) struck per 3-block
     // range into the large-prime bitmask instead of visited by every block
@@ -180,6 +184,7 @@ static int batch_alloc(gb_dev* d, Batch& b, bool with_qg) {
     CU(d, cudaEventCreate(&b.ev_k1));
     CU(d, cudaEventCreate(&b.ev_l0));
     CU(d, cudaEventCreate(&b.ev_s1));
+    CU(d, cudaEventCreateWithFlags(&b.ev_first, cudaEventDisableTiming));
     return GB_OK;
 }
 
@@ -200,6 +205,7 @@ static void batch_free(gb_dev* d, Batch& b) {
     if (b.ev_k1) cudaEventDestroy(b.ev_k1);
     if (b.ev_l0) cudaEventDestroy(b.ev_l0);
     if (b.ev_s1) cudaEventDestroy(b.ev_s1);
+    if (b.ev_first) cudaEventDestroy(b.ev_first);
     if (b.st) cudaStreamDestroy(b.st);
     b = Batch{};
 }
@@ -321,10 +327,33 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out, uint32_t* tile_
         const bool axis = large_batch_tab(b.h_jobs, n, T);
         T.cop = d->ls_cop;
         const uint64_t iLB = axis && d->iLB < d->iL1 ? d->iLB : d->iL1;
+        // First-index chain: the row walk's row 0 derives k00 from the last
+        // row-walk batch's k00 when this batch's origin lies < 2^32 wheel
+        // steps above it (consecutive claims), instead of the 64-bit
+        // remainder.  Every launch that touches a k00 buffer waits for the
+        // chain's last row-0 launch, so a buffer is never rewritten before
+        // the next batch has read it.
+        const bool rowwalk = axis && d->ls_rows && b.d_k00 != nullptr && d->d_m32 != nullptr;
+        if (d->chain_b != nullptr && d->ls_chain) CU(d, cudaStreamWaitEvent(st, d->chain_b->ev_first, 0));
+        const uint32_t* prev = nullptr;
+        uint32_t dd = 0;
+        const SegJob& j0 = b.h_jobs[0];
+        if (rowwalk && d->chain_b != nullptr && d->ls_chain && !j0.qneg && j0.qbase >= d->chain_q0 &&
+            (j0.qbase - d->chain_q0) / 6 < (1ull << 32)) {
+            prev = d->chain_b->d_k00;
+            dd = (uint32_t)((j0.qbase - d->chain_q0) / 6);
+        }
         int nl = 0;
         CU(d, launch_large_strike(b.d_jobs, n, d->d_primes, d->d_m64, d->iL0, iLB, b.d_qg, d->qg_stride, b.d_k00,
-                                  d->d_m32, axis && d->ls_rows ? &T : nullptr, &nl, st));
+                                  d->d_m32, rowwalk ? &T : nullptr, prev, dd, &nl, st));
         d->launches += nl;
+        if (rowwalk && d->ls_chain) {
+            CU(d, cudaEventRecord(b.ev_first, st));
+            d->chain_b = &b;
+            d->chain_q0 = j0.qbase;
+        } else {
+            d->chain_b = nullptr; // the per-slot path may have rewritten this batch's k00
+        }
         if (iLB < d->iL1) {
             CU(d, launch_large_batch(b.d_jobs, T, d->d_primes, d->d_m64, iLB, d->iL1, b.d_qg, d->qg_stride, st));
             d->launches++;
@@ -686,6 +715,7 @@ static int build_tables(gb_dev* d) {
         if (const char* e = getenv("GB_LB_T")) t = strtoull(e, nullptr, 0);
         if (const char* e = getenv("GB_LS_ROWS")) d->ls_rows = atoi(e) != 0;
         if (const char* e = getenv("GB_LS_COP")) d->ls_cop = (uint32_t)atoi(e);
+        if (const char* e = getenv("GB_LS_CHAIN")) d->ls_chain = atoi(e) != 0;
         if (t != 0) {
             uint64_t lo = d->iL0, hi = d->iL1; // first index with p >= t
             while (lo < hi) {

@@ -578,8 +578,10 @@ __global__ void __launch_bounds__(256) k_large_batch(const SegJob* __restrict__ 
 // this drops the per-slot remainders, folds and loop set-ups.  Rows run in
 // grid order, so the REDs of one row stay in the row's L2-resident masks.
 // FIRST: the launch of row 0 (D = 0), which computes each prime's batch
-// first index k00 itself (64-bit, first_a6 at slot 0's origin) and stores it
-// for the launch of the other rows (no separate k_large_first pass).  The
+// first index k00 itself and stores it for the launch of the other rows (no
+// separate k_large_first pass): from the previous batch's k00 when that batch
+// lay dd < 2^32 wheel steps below (k00 = k00_prev - dd mod p, one 32-bit
+// remainder; may alias k00s), else by the 64-bit first_a6 at slot 0's origin.  The
 // prime tables stream through L2 with evict-first loads, so the row's slot
 // masks stay resident for the REDs.
 template <bool FIRST>
@@ -587,8 +589,8 @@ __global__ void __launch_bounds__(256) k_large_rows(LargeBatchTab T, const SegJo
                                                     const uint32_t* __restrict__ primes,
                                                     const uint64_t* __restrict__ m64, uint64_t iL0, uint64_t iL1,
                                                     uint32_t* __restrict__ qg, uint64_t qg_stride_words,
-                                                    uint32_t* __restrict__ k00s,
-                                                    const uint32_t* __restrict__ m32s, uint32_t row0) {
+                                                    uint32_t* k00s, const uint32_t* __restrict__ m32s, uint32_t row0,
+                                                    const uint32_t* k00_prev, uint32_t dd) {
     static_assert(LS_GROUP == 2, "row walk written for two slots per row");
     // T.cop >= 1, s_cop bit x (x < 5005): gcd(x, 5*7*11*13) = 1.  A multiple q
     // of a large prime that 5, 7, 11 or 13 also divides is already clear in
@@ -633,7 +635,17 @@ __global__ void __launch_bounds__(256) k_large_rows(LargeBatchTab T, const SegJo
         const uint32_t p = __ldcs(primes + i);
         uint32_t k00, r = D; // r = D mod p (quotient of the 32-bit magic low by <= 2)
         if (FIRST) {
-            k00 = first_a6(s_j0, p, __ldcs(m64 + i));
+            if (k00_prev != nullptr) { // the previous batch's first index, dd wheel steps below
+                const uint32_t kp = __ldcs(k00_prev + (i - iL0));
+                uint32_t rd = dd;
+                if (dd >= p) {
+                    rd = dd - __umulhi(dd, __ldcs(m32s + (i - iL0))) * p;
+                    while (rd >= p) rd -= p;
+                }
+                k00 = kp >= rd ? kp - rd : kp + (p - rd);
+            } else {
+                k00 = first_a6(s_j0, p, __ldcs(m64 + i));
+            }
             __stcs(k00s + (i - iL0), k00);
         } else {
             k00 = __ldcs(k00s + (i - iL0));
@@ -2254,7 +2266,8 @@ cudaError_t launch_segment_offsets(const SegJob* jobs, uint32_t nslots, const ui
 }
 cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, const uint64_t* m64,
                                 uint64_t iL0, uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, uint32_t* k00,
-                                const uint32_t* m32, const LargeBatchTab* T, int* nlaunch, cudaStream_t st) {
+                                const uint32_t* m32, const LargeBatchTab* T, const uint32_t* k00_prev, uint32_t dd,
+                                int* nlaunch, cudaStream_t st) {
     *nlaunch = 0;
     const uint64_t np = iL1 - iL0;
     if (!np || !nslots) return cudaSuccess;
@@ -2262,11 +2275,12 @@ cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint3
     const unsigned gx = (unsigned)std::min<uint64_t>((np + 255) / 256, 148ull * 16);
     if (T != nullptr && k00 != nullptr && m32 != nullptr) { // slots on one axis: the row walk
         const unsigned rows = (nslots + LS_GROUP - 1) / LS_GROUP;
-        k_large_rows<true><<<dim3(gx, 1), 256, 0, st>>>(*T, jobs, primes, m64, iL0, iL1, qg, qg_stride_words, k00, m32, 0);
+        k_large_rows<true><<<dim3(gx, 1), 256, 0, st>>>(*T, jobs, primes, m64, iL0, iL1, qg, qg_stride_words, k00, m32, 0,
+                                                        k00_prev, dd);
         *nlaunch = 1;
         if (rows > 1) {
             k_large_rows<false><<<dim3(gx, rows - 1), 256, 0, st>>>(*T, jobs, primes, m64, iL0, iL1, qg, qg_stride_words,
-                                                                    k00, m32, 1);
+                                                                    k00, m32, 1, nullptr, 0);
             *nlaunch = 2;
         }
         return cudaGetLastError();

@@ -104,7 +104,8 @@ cudaError_t launch_segment_offsets(const SegJob* jobs, uint32_t nslots, const ui
                                    const uint64_t* m64, uint32_t iA0, uint32_t np, uint4* pmc, cudaStream_t st);
 cudaError_t launch_large_strike(const SegJob* jobs, uint32_t nslots, const uint32_t* primes, const uint64_t* m64,
                                 uint64_t iL0, uint64_t iL1, uint32_t* qg, uint64_t qg_stride_words, uint32_t* k00,
-                                const uint32_t* m32, const LargeBatchTab* T, int* nlaunch, cudaStream_t st);
+                                const uint32_t* m32, const LargeBatchTab* T, const uint32_t* k00_prev, uint32_t dd,
+                                int* nlaunch, cudaStream_t st);
 cudaError_t launch_large_batch(const SegJob* jobs, const LargeBatchTab& T, const uint32_t* primes, const uint64_t* m64,
                                uint64_t i0, uint64_t i1, uint32_t* qg, uint64_t qg_stride_words, cudaStream_t st);
 cudaError_t launch_large_m32(const uint64_t* m64, uint64_t iL0, uint64_t iL1, uint32_t* m32, cudaStream_t st);
