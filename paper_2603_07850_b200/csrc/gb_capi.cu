@@ -109,8 +109,9 @@ struct gb_dev {
     uint64_t iLB = 0;                   // first large prime of the batch walk (k_large_batch); iL1 = none
     uint32_t ls_cop = 0;                // k_large_rows skips multiples of 5..13 (1) and 17..23 (2) (GB_LS_COP; default 0: measured slower)
     Batch* chain_b = nullptr;           // batch whose k00 buffer holds the last row walk's first indices
+    Batch* last_large = nullptr;        // batch of the last large-prime launches (ev_first orders the next)
     uint64_t chain_q0 = 0;              // ... and its slot-0 origin (|Q|, positive)
-    bool ls_chain = true;               // derive k00 from chain_b's (GB_LS_CHAIN=0: 64-bit remainder per batch)
+    bool ls_chain = false;              // derive k00 from chain_b's (GB_LS_CHAIN=1; off: measured neutral, C5 0.142 s on against 0.140-0.141 s off)
     bool ls_rows = true;                // row walk (k_large_rows) for batches on one axis (GB_LS_ROWS=0: per slot)
     // mask fill (k_mask_fill): tile primes [iK0, iB1) struck per 3-block
     // range into the large-prime bitmask instead of visited by every block
@@ -330,15 +331,16 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out, uint32_t* tile_
         // First-index chain: the row walk's row 0 derives k00 from the last
         // row-walk batch's k00 when this batch's origin lies < 2^32 wheel
         // steps above it (consecutive claims), instead of the 64-bit
-        // remainder.  Every launch that touches a k00 buffer waits for the
-        // chain's last row-0 launch, so a buffer is never rewritten before
-        // the next batch has read it.
+        // remainder.  With the chain on, every large-prime launch waits for
+        // the previous one (event after its launches), so they run in
+        // submission order and a k00 buffer is never rewritten before the
+        // next batch has read it.
         const bool rowwalk = axis && d->ls_rows && b.d_k00 != nullptr && d->d_m32 != nullptr;
-        if (d->chain_b != nullptr && d->ls_chain) CU(d, cudaStreamWaitEvent(st, d->chain_b->ev_first, 0));
+        if (d->ls_chain && d->last_large != nullptr) CU(d, cudaStreamWaitEvent(st, d->last_large->ev_first, 0));
         const uint32_t* prev = nullptr;
         uint32_t dd = 0;
         const SegJob& j0 = b.h_jobs[0];
-        if (rowwalk && d->chain_b != nullptr && d->ls_chain && !j0.qneg && j0.qbase >= d->chain_q0 &&
+        if (rowwalk && d->ls_chain && d->chain_b != nullptr && !j0.qneg && j0.qbase >= d->chain_q0 &&
             (j0.qbase - d->chain_q0) / 6 < (1ull << 32)) {
             prev = d->chain_b->d_k00;
             dd = (uint32_t)((j0.qbase - d->chain_q0) / 6);
@@ -347,12 +349,12 @@ static int batch_launch(gb_dev* d, Batch& b, uint64_t* pmin_out, uint32_t* tile_
         CU(d, launch_large_strike(b.d_jobs, n, d->d_primes, d->d_m64, d->iL0, iLB, b.d_qg, d->qg_stride, b.d_k00,
                                   d->d_m32, rowwalk ? &T : nullptr, prev, dd, &nl, st));
         d->launches += nl;
-        if (rowwalk && d->ls_chain) {
+        if (d->ls_chain) {
             CU(d, cudaEventRecord(b.ev_first, st));
-            d->chain_b = &b;
+            d->last_large = &b;
+            // the per-slot path leaves no usable k00 in this batch
+            d->chain_b = rowwalk ? &b : nullptr;
             d->chain_q0 = j0.qbase;
-        } else {
-            d->chain_b = nullptr; // the per-slot path may have rewritten this batch's k00
         }
         if (iLB < d->iL1) {
             CU(d, launch_large_batch(b.d_jobs, T, d->d_primes, d->d_m64, iLB, d->iL1, b.d_qg, d->qg_stride, st));
