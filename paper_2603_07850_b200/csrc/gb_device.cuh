@@ -101,9 +101,9 @@ constexpr uint32_t TPAD = 32;                 // zero words before / after each 
 constexpr uint32_t TILE6_WORDS = 3 * TPAD + 2 * M6W; // [pad][A][pad][B][pad]
 static_assert(M6 % 32 == 0 && K6 % 32 == 0 && 6 * (M6 - K6) > PH6 + 5, "wheel-6 block geometry");
 // deep-even queue entries: t (class index in the block, < K6 + 32) | ci | window j
-constexpr int DQ_CI = K6 + 32 <= (1u << 18) ? 18 : 19;
+constexpr int DQ_CI = K6 + 64 <= (1u << 18) ? 18 : 19;
 constexpr int DQ_J = DQ_CI + 2;
-static_assert(K6 + 32 <= (1u << DQ_CI) && DQ_J + 5 <= 32, "deep queue entry layout");
+static_assert(K6 + 64 <= (1u << DQ_CI) && DQ_J + 5 <= 32, "deep queue entry layout (word entries store t0 + 32)");
 static_assert(64 * NWIN6 * 6 >= PH6, "deep windows cover the halo");
 
 // ------------------------------------------------------------- mask fill

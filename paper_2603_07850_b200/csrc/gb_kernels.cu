@@ -1239,6 +1239,62 @@ __device__ __forceinline__ uint32_t deep_round6(const uint32_t* tile, const uint
     return qn + __popc(bal);
 }
 
+#ifndef GB_DQ_WORDS
+#define GB_DQ_WORDS 1 // deep queue of word entries (0: one entry per even)
+#endif
+// Word-entry deep queue (GB_DQ_WORDS): one two-word entry per lane-word with
+// deep evens, {U = its unresolved evens, (t0 + 32) | ci << DQ_CI | j << DQ_J}
+// with t0 = the word's first class index.  Appending takes one ballot per
+// word step instead of a prefix over count thresholds and a per-even store
+// loop.  A round takes n entries; each tests ONE window j of its lowest
+// unresolved even.  A hit (or a straggler after the last window) clears that
+// even and restarts j at the class's first deep window for the next one;
+// a miss moves to window j + 1.  Entries with evens left go back.
+static_assert(QCAP >= 128, "word entries: < 32 queued + 32 appended <= QCAP / 2");
+template <bool PMIN>
+__device__ __forceinline__ uint32_t deep_round6w(const uint32_t* tile, const uint64_t* masks6, uint32_t* q,
+                                                 uint32_t qn, uint32_t n, uint32_t lane, uint32_t i0, uint32_t s,
+                                                 const SegJob& J, const Classes6& CL, const VerifyArgs& A,
+                                                 uint32_t jlim_small, K3Acc& acc) {
+    qn -= n;
+    const bool act = lane < n;
+    uint32_t U = act ? q[2 * (qn + lane)] : 0u;
+    uint32_t e = act ? q[2 * (qn + lane) + 1] : 0u;
+    __syncwarp();
+    if (lane == 0) GB_STAT(3, 1);
+    if (act) {
+        const uint32_t bit = __ffs(U) - 1;
+        const uint32_t t = (e & ((1u << DQ_CI) - 1)) - 32 + bit, ci = (e >> DQ_CI) & 3u;
+        uint32_t j = e >> DQ_J;
+        const Class6 C = CL[ci];
+        const uint32_t p = window_hit6(tile, masks6, C.r, C.G, t, j, ~0ull, ~0ull, ~0ull);
+        const uint32_t il = ci + 3 * t;
+        if (p) {
+            acc.add(p, il);
+            if constexpr (PMIN) A.pmin_out[i0 + il] = p;
+            U &= U - 1;
+            j = deep_j0(C.r);
+        } else if (j + 1 < (uint32_t)NWIN6) {
+            ++j;
+        } else {
+            push_straggler(A, J, s, i0 + il, jlim_small, 0);
+            if constexpr (PMIN) A.pmin_out[i0 + il] = 0;
+            U &= U - 1;
+            j = deep_j0(C.r);
+        }
+        e = (e & ((1u << DQ_J) - 1)) | (j << DQ_J);
+    }
+    const bool again = U != 0;
+    const uint32_t bal = __ballot_sync(0xffffffffu, again);
+    if (again) {
+        const uint32_t k = qn + __popc(bal & ((1u << lane) - 1));
+        q[2 * k] = U;
+        q[2 * k + 1] = e;
+    }
+    __syncwarp();
+    return qn + __popc(bal);
+}
+
 // bits m of window j with g = 64j + m <= gl (bit 63 - m)
 __device__ __forceinline__ uint64_t glim_mask(int64_t gl, uint32_t j) {
     const int64_t mm = gl - 64 * (int64_t)j;
@@ -1494,6 +1550,33 @@ __device__ __forceinline__ uint32_t word_deep(const uint32_t* tile, const uint64
                                               uint32_t lane, uint32_t i0, uint32_t s, const SegJob& J,
                                               const Classes6& CL, const VerifyArgs& A, uint32_t jlim_small,
                                               K3Acc& acc) {
+#if GB_DQ_WORDS
+    const uint32_t m = __ballot_sync(0xffffffffu, U != 0);
+    if (m == 0) return qn;
+#ifdef GB_STATS
+    const uint32_t tot = __reduce_add_sync(0xffffffffu, __popc(U));
+    if (lane == 0) GB_STAT(2, tot);
+#endif
+    const uint32_t ne = __popc(m);
+    if (qn + ne <= QCAP / 2) {
+        if (U) {
+            const uint32_t k = qn + __popc(m & ((1u << lane) - 1));
+            q[2 * k] = U;
+            q[2 * k + 1] = (32 * w - delta + 32) | (ci << DQ_CI) | (deep_j0(C.r) << DQ_J);
+        }
+        qn += ne;
+        __syncwarp();
+        while (qn >= 32) qn = deep_round6w<PMIN>(tile, masks6, q, qn, 32, lane, i0, s, J, CL, A, jlim_small, acc);
+    } else {
+        while (U) { // queue full (cannot happen with QCAP >= 128): in place
+            const uint32_t bit = __ffs(U) - 1;
+            U &= U - 1;
+            deep_even6<PMIN>(tile, masks6, 32 * w - delta + bit, C, ci, i0, s, J, A, jlim_small, acc);
+        }
+        __syncwarp();
+    }
+    return qn;
+#endif
     const uint32_t cnt = __popc(U);
     const uint32_t cmax = __reduce_max_sync(0xffffffffu, cnt);
     if (cmax == 0) return qn;
@@ -1726,7 +1809,11 @@ __device__ __forceinline__ void check_block(const VerifyArgs& A, const uint32_t*
             }
 #endif
         }
+#if GB_DQ_WORDS
+        while (qn) qn = deep_round6w<PMIN>(tile, masks6, q, qn, min(qn, 32u), lane, i0, s, J, CL, A, jlim_small, acc);
+#else
         while (qn) qn = deep_round6<PMIN>(tile, masks6, q, qn, min(qn, 32u), lane, i0, s, J, CL, A, jlim_small, acc);
+#endif
         if (nbatch) acc.spi += 3ull * vsum_by_index(V, FC, 1u);
         acc.sp += sp32;
     } else {
