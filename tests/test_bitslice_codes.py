@@ -51,7 +51,7 @@ def test_generated_header_matches_generator():
     hdr = os.path.join(g.ROOT, "paper_2603_07850_b200", "csrc", "gb_bitslice.cuh")
     text = open(hdr).read()
     assert "#define BS6_CODE 1" in text
-    assert "BS6_PMAX_R0 = 257" in text and "BS6_PMAX_R24 = 503" in text
-    for r, pmax in ((0, 257), (2, 503), (4, 503)):
-        code, n, _, _ = g.gen_scan6(f"bs6_scan_r{r}", r, pmax, nplanes=8, nw=g.scan6_words(503), mode="c")
+    assert "BS6_PMAX_R0 = 211" in text and "BS6_PMAX_R24 = 419" in text
+    for r, pmax in ((0, 211), (2, 419), (4, 419)):
+        code, n, _, _ = g.gen_scan6(f"bs6_scan_r{r}", r, pmax, nplanes=8, nw=g.scan6_words(419), mode="c")
         assert code in text, r

@@ -66,7 +66,7 @@ def test_low_windows(gpu, cover):
             same(dev.verify_segment(a, b), oracle.verify_segment(a, b, cover=cover))
 
 
-@pytest.mark.parametrize("p_small", [3, 5, 131, 257, 263, 8191, 8193, 8209])
+@pytest.mark.parametrize("p_small", [3, 5, 131, 211, 223, 257, 263, 419, 421, 8191, 8193, 8209])
 def test_p_small_around_the_fast_path(gpu, p_small):
     a, b = 10**9, 10**9 + 2 * 100_000
     with gpu.Device(b, p_small=p_small) as dev:

@@ -195,10 +195,10 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--shf-every", type=int, default=1)
     ap.add_argument("--pbs6", type=int, default=385, help="largest bit-sliced candidate (wheel-6 scans)")
-    ap.add_argument("--pbs-r0", type=int, default=257, help="class-0 bound (0: --pbs6)")
+    ap.add_argument("--pbs-r0", type=int, default=211, help="class-0 bound (0: --pbs6)")
     ap.add_argument("--fma-every", type=int, default=0,
                     help="every N-th candidate's funnel shift on the FMA pipe (0: none)")
-    ap.add_argument("--pbs-r24", type=int, default=503, help="classes 2/4 bound (0: --pbs6)")
+    ap.add_argument("--pbs-r24", type=int, default=419, help="classes 2/4 bound (0: --pbs6)")
     ap.add_argument("--code", choices=["z", "c"], default="c",
                     help="plane code: z = (p-3)/2, or the per-class code c (fewer plane intervals)")
     args = ap.parse_args()
