@@ -42,7 +42,11 @@ constexpr int WS_SW_LIGHT = GB_WS_SW_LIGHT, WS_SW_HEAVY = GB_WS_SW_HEAVY, WS_SW_
 // most pi(2^22) rows) since the 1.5 x 2^18 tile (1e13: 12 sieve warps 4.23 s,
 // 16 warps 4.35 s; it was 16 below 2^18-cell tiles); GB_SW=16 still selects it
 constexpr uint32_t WS_HEAVY_PRIMES = 400000;
-constexpr uint32_t WS_MASK_PRIMES = 50000; // row primes at or below: the mask split
+// row primes at or below: the 10-sieve-warp split.  Since the word-entry deep
+// queue and the 211 / 419 scan bounds, 1e12 (78 K row primes) measured
+// 0.336 s with 10 sieve warps against 0.340 s with 12, and 1e13 (216 K)
+// 4.10 s against 4.01 s (profiles/r02f_split_retune.txt)
+constexpr uint32_t WS_MASK_PRIMES = 120000;
 // warps of the group that runs the warp-cooperative strikes (max of the splits)
 constexpr int SPLIT_WARPS = WS_SW_HEAVY > WS_SW_LIGHT ? WS_SW_HEAVY : WS_SW_LIGHT;
 constexpr uint32_t P_TILE_MAX = 1u << 22; // base primes above: K_large (global strikes)
