@@ -1431,18 +1431,32 @@ __device__ __forceinline__ ClassSums class_sums(uint32_t r) {
     return S;
 }
 
+// The tile words a scan reads, WB - BS6_WORDS + 1 .. WB of each array (4 up
+// to candidate ~ 6 * 95, 3 for the lower bounds of 7-plane builds).
+#if BS6_NWORDS == 4
+#define BS6_LOAD_WORDS(a, b)                                                  \
+    const uint32_t a0 = a[-3], a1 = a[-2], a2 = a[-1], a3 = a[0];             \
+    const uint32_t b0 = b[-3], b1 = b[-2], b2 = b[-1], b3 = b[0]
+#define BS6_ARGS a0, a1, a2, a3, b0, b1, b2, b3
+#elif BS6_NWORDS == 3
+#define BS6_LOAD_WORDS(a, b)                                                  \
+    const uint32_t a0 = a[-2], a1 = a[-1], a2 = a[0];                         \
+    const uint32_t b0 = b[-2], b1 = b[-1], b2 = b[0]
+#define BS6_ARGS a0, a1, a2, b0, b1, b2
+#else
+#error "scan words per array: 3 or 4"
+#endif
+
 // Bit-sliced scan of word w of class r: U in = valid evens of the word,
 // U out = those with no candidate p <= PBS; Z = planes of the found z.
 __device__ __forceinline__ void scan_word6(const uint32_t* tile, uint32_t r, uint32_t WB, uint32_t& U,
                                            uint32_t (&Z)[NPL]) {
-    static_assert(BS6_WORDS == 4, "scan_word6 loads WB-3 .. WB of each array");
     const uint32_t* a = arr_a(tile) + WB;
     const uint32_t* b = arr_b(tile) + WB;
-    const uint32_t a0 = a[-3], a1 = a[-2], a2 = a[-1], a3 = a[0];
-    const uint32_t b0 = b[-3], b1 = b[-2], b2 = b[-1], b3 = b[0];
-    if (r == 0) bs6_scan_r0(a0, a1, a2, a3, b0, b1, b2, b3, U, Z);
-    else if (r == 2) bs6_scan_r2(a0, a1, a2, a3, b0, b1, b2, b3, U, Z);
-    else bs6_scan_r4(a0, a1, a2, a3, b0, b1, b2, b3, U, Z);
+    BS6_LOAD_WORDS(a, b);
+    if (r == 0) bs6_scan_r0(BS6_ARGS, U, Z);
+    else if (r == 2) bs6_scan_r2(BS6_ARGS, U, Z);
+    else bs6_scan_r4(BS6_ARGS, U, Z);
 }
 
 // Sums of one scanned word: sum p (weighted by the word's even index), and
@@ -1526,12 +1540,11 @@ __device__ __forceinline__ uint32_t scan_sums(const VerifyArgs& A, const uint32_
                                               uint32_t (&V)[VPL], uint32_t (&FC)[FPL], uint32_t& sp32, K3Acc& acc) {
     const uint32_t* a = arr_a(tile) + WB;
     const uint32_t* b = arr_b(tile) + WB;
-    const uint32_t a0 = a[-3], a1 = a[-2], a2 = a[-1], a3 = a[0];
-    const uint32_t b0 = b[-3], b1 = b[-2], b2 = b[-1], b3 = b[0];
+    BS6_LOAD_WORDS(a, b);
     uint32_t U = valid, Z[NPL];
-    if constexpr (R == 0) bs6_scan_r0(a0, a1, a2, a3, b0, b1, b2, b3, U, Z);
-    else if constexpr (R == 2) bs6_scan_r2(a0, a1, a2, a3, b0, b1, b2, b3, U, Z);
-    else bs6_scan_r4(a0, a1, a2, a3, b0, b1, b2, b3, U, Z);
+    if constexpr (R == 0) bs6_scan_r0(BS6_ARGS, U, Z);
+    else if constexpr (R == 2) bs6_scan_r2(BS6_ARGS, U, Z);
+    else bs6_scan_r4(BS6_ARGS, U, Z);
     ClassSums CS;
     CS.kz0 = R == 2 ? 2u : 4u;
     CS.kf = R == 4 ? 0xFFFFFFFFu : 1u;

@@ -241,6 +241,7 @@ def main():
     parts.append(f"constexpr uint32_t BS6_PMAX = {pmax};")
     parts.append(f"constexpr int BS6_PLANES = {npl};")
     parts.append(f"constexpr int BS6_WORDS = {nw};    // tile words per array a scan reads (WB-{nw - 1} .. WB)")
+    parts.append(f"#define BS6_NWORDS {nw} // the same for the preprocessor (scan call sites)")
     parts.append("")
     parts.append("} // namespace gbk")
     with open(OUT, "w") as f:
