@@ -809,6 +809,10 @@ __device__ __forceinline__ void strike_warp6(uint32_t* arr, uint32_t o, uint32_t
 // TPAD >= 32 zero words past the array (word M6W + lane at most; distinct
 // banks across the warp), where clearing a bit of a zero word is a no-op.
 static_assert(TPAD >= 32, "branch-free strikes need 32 pad words past each array");
+#ifndef GB_STRIKE_IMAD
+#define GB_STRIKE_IMAD 1
+#endif
+__constant__ uint32_t c_four = 4; // not a compile-time constant: keeps (w * 4 + base) an IMAD
 __device__ __forceinline__ void strike_if(uint32_t* arr, uint32_t c, uint32_t lane) {
 #if GB_PRED_STRIKE == 2
     // predicated RED: a miss issues the instruction but moves no data
@@ -816,6 +820,13 @@ __device__ __forceinline__ void strike_if(uint32_t* arr, uint32_t c, uint32_t la
     const uint32_t a = (uint32_t)__cvta_generic_to_shared(arr) + ((c >> 3) & ~3u);
     asm volatile("{\n\t.reg .pred p;\n\tsetp.lt.u32 p, %0, %1;\n\t@p red.shared.and.b32 [%2], %3;\n\t}"
                  ::"r"(c), "r"(M6), "r"(a), "r"(__funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, c)) : "memory");
+#elif GB_PRED_STRIKE && GB_STRIKE_IMAD
+    // word address as one IMAD with a constant-bank 4: the multiply runs on
+    // the FMA pipe instead of a shift, mask and add on the ALU pipe (the
+    // kernel's binding pipe)
+    const uint32_t cc = min(c, M6 + 32 * lane);
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(arr) + (cc >> 5) * c_four;
+    asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(a), "r"(__funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, cc)) : "memory");
 #elif GB_PRED_STRIKE
     strike(arr, min(c, M6 + 32 * lane));
 #else
