@@ -813,6 +813,7 @@ static_assert(TPAD >= 32, "branch-free strikes need 32 pad words past each array
 #define GB_STRIKE_IMAD 1
 #endif
 __constant__ uint32_t c_four = 4; // not a compile-time constant: keeps (w * 4 + base) an IMAD
+__constant__ uint32_t c_2p27 = 1u << 27; // likewise keeps c >> 5 an IMAD.HI (GB_STRIKE_IMAD=2)
 __device__ __forceinline__ void strike_if(uint32_t* arr, uint32_t c, uint32_t lane) {
 #if GB_PRED_STRIKE == 2
     // predicated RED: a miss issues the instruction but moves no data
@@ -825,7 +826,12 @@ __device__ __forceinline__ void strike_if(uint32_t* arr, uint32_t c, uint32_t la
     // the FMA pipe instead of a shift, mask and add on the ALU pipe (the
     // kernel's binding pipe)
     const uint32_t cc = min(c, M6 + 32 * lane);
+#if GB_STRIKE_IMAD >= 2
+    // cc >> 5 as the high word of cc * 2^27: IMAD.HI, also on the FMA pipe
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(arr) + __umulhi(cc, c_2p27) * c_four;
+#else
     const uint32_t a = (uint32_t)__cvta_generic_to_shared(arr) + (cc >> 5) * c_four;
+#endif
     asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(a), "r"(__funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, cc)) : "memory");
 #elif GB_PRED_STRIKE
     strike(arr, min(c, M6 + 32 * lane));
@@ -834,11 +840,21 @@ __device__ __forceinline__ void strike_if(uint32_t* arr, uint32_t c, uint32_t la
 #endif
 }
 
+#if GB_STRIKE_IMAD >= 3
+// strike with the word address on the FMA pipe (IMAD.HI + IMAD)
+__device__ __forceinline__ void strike6(uint32_t* arr, uint32_t c) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(arr) + __umulhi(c, c_2p27) * c_four;
+    asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(a), "r"(__funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, c)) : "memory");
+}
+#else
+__device__ __forceinline__ void strike6(uint32_t* arr, uint32_t c) { strike(arr, c); }
+#endif
+
 // strikes c, c + step, ... < M6 of one class array (two per trip)
 __device__ __forceinline__ void strike_run6(uint32_t* arr, uint32_t c, uint32_t step, uint32_t lane) {
     while (c + step < M6) {
-        strike(arr, c);
-        strike(arr, c + step);
+        strike6(arr, c);
+        strike6(arr, c + step);
         c += 2 * step;
     }
     strike_if(arr, c, lane);
