@@ -36,13 +36,16 @@ __device__ unsigned long long g_stats[8];
 #define GB_STAT(i, v) ((void)0)
 #endif
 
-// single-strike rows loaded before their strikes, by sieve-group size: the
-// light split (12 sieve warps) hides the L2 latency with more rows per warp
+// single-strike rows loaded before their strikes, by sieve-group size.  Since
+// the IMAD-addressed strikes (17 instructions per row) 12 rows per thread
+// measured best for the 12-warp split (1e13 3.88 s; 8 / 10 / 16 / 20: 3.89 /
+// 3.89 / 3.93 / 3.93 s); 1e12 (10 sieve warps, the HEAVY value) is flat over
+// 8 / 12 / 16 (profiles/r02f_rows_inflight_ab.txt)
 #ifndef GB_RUN_INFLIGHT
 #define GB_RUN_INFLIGHT 4 // run-prime rows loaded before their strikes
 #endif
 #ifndef GB_SS_INFLIGHT_LIGHT
-#define GB_SS_INFLIGHT_LIGHT 16
+#define GB_SS_INFLIGHT_LIGHT 12
 #endif
 #ifndef GB_SS_INFLIGHT_HEAVY
 #define GB_SS_INFLIGHT_HEAVY 12
