@@ -817,6 +817,9 @@ static_assert(TPAD >= 32, "branch-free strikes need 32 pad words past each array
 #endif
 __constant__ uint32_t c_four = 4; // not a compile-time constant: keeps (w * 4 + base) an IMAD
 __constant__ uint32_t c_2p27 = 1u << 27; // likewise keeps c >> 5 an IMAD.HI (GB_STRIKE_IMAD=2)
+#ifndef GB_RUN_IMAD
+#define GB_RUN_IMAD 1 // run-loop strikes: word address as shift + IMAD (1e12 0.333 -> 0.328 s, 1e13 3.87 -> 3.82 s)
+#endif
 __device__ __forceinline__ void strike_if(uint32_t* arr, uint32_t c, uint32_t lane) {
 #if GB_PRED_STRIKE == 2
     // predicated RED: a miss issues the instruction but moves no data
@@ -843,7 +846,14 @@ __device__ __forceinline__ void strike_if(uint32_t* arr, uint32_t c, uint32_t la
 #endif
 }
 
-#if GB_STRIKE_IMAD >= 3
+#if GB_RUN_IMAD
+// run-loop strike with the word address as shift + IMAD (FMA pipe) instead of
+// shift + mask + add
+__device__ __forceinline__ void strike6(uint32_t* arr, uint32_t c) {
+    const uint32_t a = (uint32_t)__cvta_generic_to_shared(arr) + (c >> 5) * c_four;
+    asm volatile("red.shared.and.b32 [%0], %1;" ::"r"(a), "r"(__funnelshift_l(0xFFFFFFFEu, 0xFFFFFFFEu, c)) : "memory");
+}
+#elif GB_STRIKE_IMAD >= 3
 // strike with the word address on the FMA pipe (IMAD.HI + IMAD)
 __device__ __forceinline__ void strike6(uint32_t* arr, uint32_t c) {
     const uint32_t a = (uint32_t)__cvta_generic_to_shared(arr) + __umulhi(c, c_2p27) * c_four;
